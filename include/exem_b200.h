@@ -1,0 +1,231 @@
+/*
+ * exem_b200.h -- C-ABI of the B200-native exemplar-clustering evaluator.
+ *
+ * Drop-in boundary for the evaluation path of the reference package
+ * `exembatch` (arXiv 2101.08763 re-implementation).  The reference binds no
+ * native code: its plugin point is the backend string dispatch in
+ * pkg/src/exembatch/evaluate.py:42,59-65,282-293 plus the batch dissimilarity
+ * pkg/src/exembatch/objective.py:24-61,75-90.  Every function below replaces
+ * one numeric step of that Python path (file:line cited per entry point);
+ * the Python package `paper_2101_08763_b200` binds them with ctypes exactly
+ * as INTEGRATION.md shows.
+ *
+ * Conventions
+ *  - Plain pointers + sizes only.  Every pointer argument is DEVICE memory
+ *    owned by the caller unless stated otherwise; nothing is retained across
+ *    calls and the library allocates no persistent device memory.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default).
+ *    All calls are asynchronous and stream-ordered; none synchronises.
+ *  - Return value is an EXEM_* status; exem_last_error() gives a
+ *    thread-local message for the last non-zero status.
+ *  - Device layouts:
+ *      SIMT layout  vt[d_pad][ld]  column-major points (the reference's
+ *                   F-order, pkg/src/exembatch/core.py:286), compute type
+ *                   float (f16/bf16/f32 storage) or double (f64), zero padded.
+ *      TC layout    x[rows][kp]    point-major, K-contiguous half operand
+ *                   (bf16/f16) with d data columns followed by 6 folded
+ *                   constant columns; TMA 128B-swizzle friendly.
+ */
+#ifndef EXEM_B200_H
+#define EXEM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- dtype tags (Precision, pkg/src/exembatch/core.py:33-94; +bf16) ---- */
+#define EXEM_F16 0
+#define EXEM_BF16 1
+#define EXEM_F32 2
+#define EXEM_F64 3
+
+/* ---- status codes -> pkg/src/exembatch/errors.py:4-41 ---- */
+#define EXEM_OK 0
+#define EXEM_ERR_ARG 1         /* ValueError / DimensionMismatchError        */
+#define EXEM_ERR_OOM 2         /* OutOfMemoryError (errors.py:28)            */
+#define EXEM_ERR_CUDA 3        /* ExemError (CUDA launch / runtime failure)  */
+#define EXEM_ERR_DATA 4        /* InvalidDataError (errors.py:20)            */
+#define EXEM_ERR_UNSUPPORTED 5 /* ExemError: no sm_100a device / bad dtype   */
+
+const char *exem_last_error(void);
+int exem_abi_version(void);
+
+/* Device query: SM count, compute capability, opt-in shared memory. */
+int exem_device_info(int device, int *sm_count, int *cc_major, int *cc_minor,
+                     int64_t *smem_optin);
+
+/* ---- layout helpers (pure host arithmetic, no device work) ---- */
+int64_t exem_pad_points(int64_t n);          /* ld of the SIMT layout        */
+int64_t exem_pad_dims(int64_t d);            /* d_pad of the SIMT layout     */
+int64_t exem_split_points(int64_t n);        /* points per partial-sum split */
+int64_t exem_num_splits(int64_t n);          /* ceil(n / split_points)       */
+int64_t exem_tc_kp(int64_t d);               /* K stride of the TC operand   */
+int64_t exem_tc_rows(int64_t n);             /* row count of the TC operand  */
+int64_t exem_reduce_scratch(int64_t count);  /* doubles of scratch needed by
+                                                the fixed-order reductions  */
+
+/*
+ * K1  ground_prepare
+ * Replaces build_ground_set's numeric part, pkg/src/exembatch/core.py:286-309
+ * (storage cast, aux_distances = d(v_i, e0), aux sum).
+ *   src      [d][n] column-major storage-dtype values (the F-order buffer,
+ *            GroundSet.data core.py:152-155), device.
+ *   e0       [d] storage-dtype auxiliary vector, device.
+ *   vt       out [d_pad][ld] compute-type SIMT layout (zero padded).
+ *   norms    out [ld] double, ||v_i||^2 of the stored values (0 on padding).
+ *   aux      out [ld] compute type, d(v_i, e0) rounded through the storage
+ *            dtype (the reference stores aux_distances at dt, core.py:304).
+ *   aux_sum  out [1] double, sum_i aux_i in fixed order.
+ *   scratch  exem_reduce_scratch(n) doubles.
+ */
+int exem_ground_prepare(int dtype, const void *src, int64_t n, int64_t d,
+                        const void *e0, void *vt, int64_t ld, double *norms,
+                        void *aux, double *aux_sum, double *scratch,
+                        void *stream);
+
+/*
+ * K2  set_min -- per-point minimum over one explicit element set
+ * Replaces min_distances, pkg/src/exembatch/objective.py:113-141, and the
+ * sum inside _set_value, pkg/src/exembatch/evaluate.py:105-112.
+ *   elems    [k][d_pad] compute-type element rows (device).
+ *   enorms   [k] double ||e||^2.
+ *   include_aux  1: t_i = min(aux_i, min_e d) (objective.py:138-139).
+ *   t_out    optional [n] compute type (NULL to skip).
+ *   label_out optional [n] int64 argmin element, lowest index on ties
+ *            (assign_clusters, pkg/src/exembatch/optimize.py:115-136).
+ *   sum_out  optional [1] double fixed-order sum_i t_i.
+ */
+int exem_set_min(int dtype, const void *vt, int64_t ld, int64_t n, int64_t d,
+                 const double *norms, const void *aux, const void *elems,
+                 const double *enorms, int64_t k, int include_aux, void *t_out,
+                 int64_t *label_out, double *sum_out, double *scratch,
+                 void *stream);
+
+/*
+ * K4  batch_eval -- explicit packed sets (the paper's S_multi)
+ * Replaces evaluate_batch / _reference_eval / tiled_evaluate,
+ * pkg/src/exembatch/evaluate.py:142-149,197-270,273-293, over the packed
+ * round-robin layout of pack_batch, pkg/src/exembatch/core.py:331-346:
+ *   packed   [d_pad][k_max][l_pad] compute type; value (j,e,dim) at
+ *            dim*(k_max*l_pad) + e*l_pad + j  (packed_address, core.py:320).
+ *   pnorms   [k_max][l_pad] double ||S_j[e]||^2.
+ *   card     [l] int32 cardinalities; slots e >= card[j] are never used.
+ *   partial  out [splits][l] double, sum over the split's points of
+ *            t_i(S_j) = min(aux_i, min_e d(v_i, S_j[e])).
+ *   split_pts  points per partial-sum split (exem_split_points of the
+ *            GLOBAL n); a row shard / streamed slice of V must start on a
+ *            split boundary, so per-set sums never depend on sharding.
+ *   splits   ceil(n / split_pts) for the n points passed here.
+ */
+int exem_batch_eval(int dtype, const void *vt, int64_t ld, int64_t n,
+                    int64_t d, const double *norms, const void *aux,
+                    const void *packed, const double *pnorms,
+                    const int32_t *card, int64_t l, int64_t l_pad,
+                    int64_t k_max, int64_t split_pts, double *partial,
+                    int64_t splits, void *stream);
+
+/*
+ * K3  greedy_gains -- optimizer-aware batched evaluation of every
+ * S u {c} of one Greedy step in one launch
+ * Replaces the batch built and evaluated in greedy_maximize,
+ * pkg/src/exembatch/optimize.py:61-71 (via evaluate.py:142-149).
+ * Computes G_c = sum_i max(0, m_i - d(v_i, c)) for every candidate row c,
+ * with m_i = min(aux_i, min_{s in S} d(v_i, s)) held on device.
+ * SIMT form (f32/f64):
+ *   cvt      [d_pad][ldc] candidate SIMT layout (== vt for Greedy).
+ *   cnorms   [ldc] double ||c||^2.
+ *   vt/norms/m  point shard (SIMT layout), m in compute type.
+ *   partial  out [splits][l] double.
+ */
+int exem_greedy_gains_simt(int dtype, const void *cvt, int64_t ldc,
+                           const double *cnorms, int64_t l, const void *vt,
+                           int64_t ld, const double *norms, const void *m,
+                           int64_t n, int64_t d, int64_t split_pts,
+                           double *partial, int64_t splits, void *stream);
+
+/*
+ * K3-TC  tcgen05 form (bf16/f16 operands, fp32 TMEM accumulators):
+ *   xc   [tc_rows(l)][kp] candidate operand rows  [c, 1,1,1, -b_hi,-b_mid,-b_lo]
+ *   xp   [tc_rows(n)][kp] point operand rows      [v, -h_hi,-h_mid,-h_lo, 1,1,1]
+ *   with b = ||c||^2/2 and h_i = (||v_i||^2 - m_i)/2, so one MMA row-dot is
+ *   D = (m_i - d(v_i,c))/2; partial receives sum_i max(0, D) * 2.
+ */
+int exem_greedy_gains_tc(int dtype, const void *xc, int64_t l, const void *xp,
+                         int64_t n, int64_t d, int64_t split_pts,
+                         double *partial, int64_t splits, void *stream);
+
+/* Build the TC candidate operand from the SIMT layout (+ norms). */
+int exem_tc_pack_candidates(int dtype, const void *vt, int64_t ld, int64_t n,
+                            int64_t d, const double *norms, void *xc,
+                            void *stream);
+/* Build / refresh the TC point operand from the SIMT layout, norms and m. */
+int exem_tc_pack_points(int dtype, const void *vt, int64_t ld, int64_t n,
+                        int64_t d, const double *norms, const void *m,
+                        void *xp, void *stream);
+
+/*
+ * K6  reduce_partials: G[j] = scale * sum_{s} partial[s][j], fixed order.
+ * Replaces np.sum(t, dtype=acc) per set, pkg/src/exembatch/evaluate.py:111.
+ */
+int exem_reduce_partials(const double *partial, int64_t splits, int64_t l,
+                         double scale, double *out, void *stream);
+
+/*
+ * K5  argmax_select: masked argmax over G (first maximum = lowest index,
+ * pkg/src/exembatch/optimize.py:73), marks it selected, appends it to the
+ * device-resident trajectory: sel_idx[step], sel_gain[step].
+ *   selected  [l] uint8 mask (1 = already in S, excluded).
+ *   index_map optional [l] int64 candidate row -> ground index (NULL: identity)
+ */
+int exem_argmax_select(const double *gains, int64_t l, uint8_t *selected,
+                       const int64_t *index_map, int64_t step,
+                       int64_t *sel_idx, double *sel_gain, double *scratch,
+                       void *stream);
+
+/*
+ * K2  greedy_update: m_i <- min(m_i, d(v_i, c*)) for c* = sel_idx[step]
+ * (the exemplar just chosen, read on device -- no host round trip), and
+ * msum[step] = sum_i m_i (fixed order) -- pkg/src/exembatch/optimize.py:74-76.
+ *   cvt/ldc   candidate SIMT layout the index refers to.
+ *   xp/kp     optional TC point operand (NULL for f32/f64): its folded -h
+ *             columns are rewritten from the new m_i.
+ */
+int exem_greedy_update(int dtype, const void *vt, int64_t ld, int64_t n,
+                       int64_t d, const double *norms, const void *cvt,
+                       int64_t ldc, const double *cnorms,
+                       const int64_t *sel_idx, int64_t step, void *m,
+                       void *xp, int64_t kp, double *msum, double *scratch,
+                       void *stream);
+
+/* m_i <- aux_i (start of a Greedy run); msum_out = sum aux (fixed order). */
+int exem_greedy_init(int dtype, const void *aux, int64_t n, void *m,
+                     double *msum_out, double *scratch, void *stream);
+
+/*
+ * Distance matrix for Dissimilarity.distances / _squared_euclidean_batch,
+ * pkg/src/exembatch/objective.py:42-61,75-90:  out[i][j] = d(a_i, b_j).
+ *   a [m][d_pad], b [q][d_pad] compute type row-major; out [m][q] compute.
+ */
+int exem_distance_matrix(int dtype, const void *a, const double *anorms,
+                         int64_t m, const void *b, const double *bnorms,
+                         int64_t q, int64_t d, int64_t d_pad, void *out,
+                         void *stream);
+
+/* pnorms[e][j] = ||S_j[e]||^2 of a packed [d_pad][k_max][l_pad] batch
+ * (the element norms e2 of objective.py:84, computed once per batch). */
+int exem_packed_norms(int dtype, const void *packed, int64_t d, int64_t k_max,
+                      int64_t l_pad, double *out, void *stream);
+
+/* Row norms ||x_r||^2 (double) of a [rows][d_pad] compute-type matrix. */
+int exem_row_norms(int dtype, const void *x, int64_t rows, int64_t d,
+                   int64_t d_pad, double *out, void *stream);
+
+/* Number of kernels this library launched since load (evidence counter). */
+int64_t exem_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EXEM_B200_H */

@@ -1,0 +1,916 @@
+// exem_simt.cu -- CUDA-core (FFMA/DFMA) kernels for sm_100a and their
+// C-ABI entry points.
+//
+//   K1 ground_prepare   core.py:286-309        (HBM-bound)
+//   K2 set_min / greedy_update / greedy_init  objective.py:113-141,
+//                       evaluate.py:105-112, optimize.py:74-76 (HBM-bound)
+//   K3 greedy_gains_simt  optimize.py:61-71    (FFMA/DFMA-bound)
+//   K4 batch_eval       evaluate.py:142-149,197-270 over pack_batch layout
+//                       core.py:331-346        (FFMA/DFMA-bound)
+//   K5 argmax_select    optimize.py:73-76      (latency)
+//   K6 reduce_partials  evaluate.py:111        (HBM/latency)
+//
+// All sums are accumulated in fp64 with a fixed reduction order, so every
+// output is bit-reproducible for a given (n, split_pts) -- the analogue of the
+// reference's fixed COL_BLOCK sweep (core.py:27-30).
+#include <cfloat>
+
+#include "exem_common.cuh"
+
+namespace exem {
+
+static thread_local char g_err[1024] = "";
+static unsigned long long g_launches = 0;
+
+void set_error(const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+int fail(int code, const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+void count_launch() { __atomic_add_fetch(&g_launches, 1ull, __ATOMIC_RELAXED); }
+
+constexpr int kRedThreads = 256;
+
+// Final fixed-order reduction of block partials (one block).
+__global__ void __launch_bounds__(1024)
+    reduce_fixed_kernel(const double *__restrict__ in, int64_t count,
+                        double *__restrict__ out, int64_t out_index) {
+  __shared__ double sh[32];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < count; i += blockDim.x) s += in[i];
+  double r = block_sum<1024>(s, sh);
+  if (threadIdx.x == 0) out[out_index] = r;
+}
+
+static int reduce_fixed(const double *partials, int64_t count, double *out,
+                        int64_t out_index, cudaStream_t st) {
+  reduce_fixed_kernel<<<1, 1024, 0, st>>>(partials, count, out, out_index);
+  EXEM_LAUNCH_CHECK("reduce_fixed_kernel");
+  return EXEM_OK;
+}
+
+// ============================================================ K1 prepare
+template <int DT>
+__global__ void __launch_bounds__(kRedThreads)
+    ground_prepare_kernel(const typename Traits<DT>::S *__restrict__ src,
+                          int64_t n, int d, int d_pad,
+                          const typename Traits<DT>::S *__restrict__ e0,
+                          typename Traits<DT>::C *__restrict__ vt, int64_t ld,
+                          double *__restrict__ norms,
+                          typename Traits<DT>::C *__restrict__ aux,
+                          double *__restrict__ partials) {
+  using S = typename Traits<DT>::S;
+  using C = typename Traits<DT>::C;
+  __shared__ double sh[32];
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double nrm = 0.0, dst = 0.0;
+  if (i < ld) {
+    for (int k = 0; k < d_pad; ++k) {
+      C x = C(0);
+      if (k < d && i < n) x = to_c(src[(int64_t)k * n + i]);
+      vt[(int64_t)k * ld + i] = x;
+      if (k < d && i < n) {
+        double xd = (double)x;
+        nrm += xd * xd;
+        double df = xd - (double)to_c(e0[k]);
+        dst += df * df;
+      }
+    }
+    // aux_distances are stored at the storage dtype (core.py:303-305).
+    C a = (i < n) ? to_c(from_d<S>(dst)) : C(0);
+    if (i < n) {
+      norms[i] = nrm;
+      aux[i] = a;
+    } else {
+      norms[i] = 0.0;
+      aux[i] = C(0);
+    }
+    dst = (i < n) ? (double)a : 0.0;
+  }
+  double r = block_sum<kRedThreads>(dst, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = r;
+}
+
+// ============================================================ K2 set_min
+// One thread per point; the set's elements are staged through shared memory
+// in chunks of kSetChunk rows and each thread keeps kSetChunk dot products in
+// registers, so V is streamed ceil(k / kSetChunk) times (HBM-bound).
+constexpr int kSetChunk = 8;
+
+template <int DT>
+__global__ void __launch_bounds__(kRedThreads)
+    set_min_kernel(const typename Traits<DT>::C *__restrict__ vt, int64_t ld,
+                   int64_t n, int d, const double *__restrict__ norms,
+                   const typename Traits<DT>::C *__restrict__ aux,
+                   const typename Traits<DT>::C *__restrict__ elems, int d_pad,
+                   const double *__restrict__ enorms, int k, int include_aux,
+                   typename Traits<DT>::C *__restrict__ t_out,
+                   int64_t *__restrict__ label_out,
+                   double *__restrict__ partials) {
+  using C = typename Traits<DT>::C;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C *se = reinterpret_cast<C *>(smem_raw);  // [kSetChunk][d_pad]
+  __shared__ double sh[32];
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = i < n;
+  const C ai = live ? (C)norms[i] : C(0);
+  C best = tinf<C>();
+  int64_t lab = 0;
+  for (int e0 = 0; e0 < k; e0 += kSetChunk) {
+    const int ec = min(kSetChunk, k - e0);
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < ec * d_pad; idx += blockDim.x)
+      se[idx] = elems[(int64_t)e0 * d_pad + idx];
+    __syncthreads();
+    C acc[kSetChunk];
+#pragma unroll
+    for (int e = 0; e < kSetChunk; ++e) acc[e] = C(0);
+    if (live) {
+      for (int kk = 0; kk < d; ++kk) {
+        const C x = vt[(int64_t)kk * ld + i];
+#pragma unroll
+        for (int e = 0; e < kSetChunk; ++e) {
+          if (Traits<DT>::kDirect) {
+            const C df = x - se[e * d_pad + kk];
+            acc[e] = fma(df, df, acc[e]);
+          } else {
+            acc[e] = fma(x, se[e * d_pad + kk], acc[e]);
+          }
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < kSetChunk; ++e) {
+        if (e < ec) {
+          C dist = Traits<DT>::kDirect
+                       ? acc[e]
+                       : gemm_form<C>(acc[e], ai, (C)enorms[e0 + e]);
+          if (dist < best) {  // strict: lowest element index wins ties
+            best = dist;
+            lab = e0 + e;
+          }
+        }
+      }
+    }
+  }
+  C t = best;
+  if (include_aux && live) t = tmin(t, aux[i]);
+  if (live) {
+    if (t_out) t_out[i] = t;
+    if (label_out) label_out[i] = lab;
+  }
+  double r = block_sum<kRedThreads>(live ? (double)t : 0.0, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = r;
+}
+
+// ============================================================ greedy m init
+template <typename C>
+__global__ void __launch_bounds__(kRedThreads)
+    greedy_init_kernel(const C *__restrict__ aux, int64_t n, C *__restrict__ m,
+                       double *__restrict__ partials) {
+  __shared__ double sh[32];
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double v = 0.0;
+  if (i < n) {
+    m[i] = aux[i];
+    v = (double)aux[i];
+  }
+  double r = block_sum<kRedThreads>(v, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = r;
+}
+
+// ============================================================ K2 greedy update
+// m_i <- min(m_i, d(v_i, c*)), c* read from sel_idx[step] on device.
+// Optionally refreshes the TC point operand's folded -h columns.
+template <int DT>
+__global__ void __launch_bounds__(kRedThreads)
+    greedy_update_kernel(const typename Traits<DT>::C *__restrict__ vt,
+                         int64_t ld, int64_t n, int d,
+                         const double *__restrict__ norms,
+                         const typename Traits<DT>::C *__restrict__ cvt,
+                         int64_t ldc, const double *__restrict__ cnorms,
+                         const int64_t *__restrict__ sel_idx, int64_t step,
+                         typename Traits<DT>::C *__restrict__ m,
+                         typename Traits<DT>::S *__restrict__ xp, int64_t kp,
+                         double *__restrict__ partials) {
+  using C = typename Traits<DT>::C;
+  using S = typename Traits<DT>::S;
+  __shared__ double sh[32];
+  const int64_t c = sel_idx[step];
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double v = 0.0;
+  if (i < n) {
+    C acc = C(0);
+    for (int kk = 0; kk < d; ++kk) {
+      const C x = vt[(int64_t)kk * ld + i];
+      const C y = cvt[(int64_t)kk * ldc + c];
+      if (Traits<DT>::kDirect) {
+        const C df = x - y;
+        acc = fma(df, df, acc);
+      } else {
+        acc = fma(x, y, acc);
+      }
+    }
+    C dist = Traits<DT>::kDirect
+                 ? acc
+                 : gemm_form<C>(acc, (C)norms[i], (C)cnorms[c]);
+    C mi = tmin(m[i], dist);
+    m[i] = mi;
+    v = (double)mi;
+    if (xp != nullptr) {
+      // h_i = (||v_i||^2 - m_i)/2 split into three half pieces (~24 bits).
+      double h = 0.5 * (norms[i] - (double)mi);
+      S h0 = from_d<S>(h);
+      double r1 = h - (double)to_c(h0);
+      S h1 = from_d<S>(r1);
+      S h2 = from_d<S>(r1 - (double)to_c(h1));
+      S *row = xp + i * kp + d;
+      row[0] = from_d<S>(-(double)to_c(h0));
+      row[1] = from_d<S>(-(double)to_c(h1));
+      row[2] = from_d<S>(-(double)to_c(h2));
+    }
+  }
+  double r = block_sum<kRedThreads>(v, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = r;
+}
+
+// ============================================================ K3 / K4 SIMT
+// Register-blocked outer product: CTA tile 128 rows (candidates / sets) x
+// 128 points, 256 threads, 8x8 per thread, k-chunks of 8 double-buffered
+// with cp.async.  Row r of the thread tile maps to tile row
+// (r<4 ? ty*4+r : 64+ty*4+r-4); same for columns with tx.
+constexpr int kBM = 128, kBN = 128, kBK = 8, kThreads = 256;
+
+template <typename T>
+struct SimtSmem {
+  T a[2][kBK][kBM];
+  T b[2][kBK][kBN];
+};
+
+template <typename T>
+__device__ __forceinline__ void load_chunk(T (*dst)[kBM], const T *src,
+                                           int64_t ldsrc, int64_t col0,
+                                           int k0) {
+  constexpr int kVec = 16 / sizeof(T);            // elements per 16B
+  constexpr int kPerRow = kBM / kVec;             // 16B packets per row
+  constexpr int kTotal = kBK * kPerRow;           // packets per chunk
+#pragma unroll
+  for (int p = threadIdx.x; p < kTotal; p += kThreads) {
+    const int row = p / kPerRow, col = (p % kPerRow) * kVec;
+    cp_async16(&dst[row][col], src + (int64_t)(k0 + row) * ldsrc + col0 + col);
+  }
+}
+
+template <typename T, bool kDirect>
+__device__ __forceinline__ void mma_chunk(const SimtSmem<T> &sm, int buf,
+                                          int tx, int ty, T (&acc)[8][8]) {
+#pragma unroll
+  for (int kk = 0; kk < kBK; ++kk) {
+    T a[8], b[8];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      a[r] = sm.a[buf][kk][ty * 4 + r];
+      a[4 + r] = sm.a[buf][kk][64 + ty * 4 + r];
+      b[r] = sm.b[buf][kk][tx * 4 + r];
+      b[4 + r] = sm.b[buf][kk][64 + tx * 4 + r];
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        if (kDirect) {
+          const T df = a[r] - b[c];
+          acc[r][c] = fma(df, df, acc[r][c]);
+        } else {
+          acc[r][c] = fma(a[r], b[c], acc[r][c]);
+        }
+      }
+  }
+}
+
+// Full-k mainloop for one (row tile, point tile) pair.
+template <typename T, bool kDirect>
+__device__ __forceinline__ void simt_mainloop(SimtSmem<T> &sm, const T *arow,
+                                              int64_t lda, int64_t a0,
+                                              const T *bpts, int64_t ldb,
+                                              int64_t b0, int d_pad, int tx,
+                                              int ty, T (&acc)[8][8]) {
+  const int nk = d_pad / kBK;
+  __syncthreads();  // previous consumers of both buffers are done
+  load_chunk<T>(sm.a[0], arow, lda, a0, 0);
+  load_chunk<T>(sm.b[0], bpts, ldb, b0, 0);
+  cp_async_commit();
+  for (int c = 0; c < nk; ++c) {
+    if (c + 1 < nk) {
+      load_chunk<T>(sm.a[(c + 1) & 1], arow, lda, a0, (c + 1) * kBK);
+      load_chunk<T>(sm.b[(c + 1) & 1], bpts, ldb, b0, (c + 1) * kBK);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    mma_chunk<T, kDirect>(sm, c & 1, tx, ty, acc);
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ int tile_off(int t4, int r) {
+  return r < 4 ? t4 * 4 + r : 64 + t4 * 4 + (r - 4);
+}
+
+// K3: partial[s][c] = sum_{i in split s} max(0, c.v_i - h_i - b'_c),
+//     h_i = (a_i - m_i)/2, b'_c = ||c||^2/2  => 2*that = sum max(0, m_i - d).
+// The per-tile constants live in shared memory to keep the 8x8 register
+// tile spill-free at 2 CTAs/SM.
+template <typename T, int kMinBlocks>
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
+    gains_simt_kernel(const T *__restrict__ cvt, int64_t ldc,
+                      const double *__restrict__ cnorms, int64_t l,
+                      const T *__restrict__ vt, int64_t ld,
+                      const double *__restrict__ norms,
+                      const T *__restrict__ m, int64_t n, int d_pad,
+                      int64_t split_pts, double *__restrict__ partial) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SimtSmem<T> &sm = *reinterpret_cast<SimtSmem<T> *>(smem_raw);
+  __shared__ T s_b[kBM];
+  __shared__ T s_h[kBN];
+  const int tid = threadIdx.x;
+  const int tx = tid % 16, ty = tid / 16;
+  const int64_t c0 = (int64_t)blockIdx.x * kBM;
+  const int64_t split = blockIdx.y;
+  const int64_t p_begin = split * split_pts;
+  const int64_t p_end = min(n, p_begin + split_pts);
+
+  if (tid < kBM) s_b[tid] = (c0 + tid < l) ? (T)(0.5 * cnorms[c0 + tid]) : T(0);
+  double g[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) g[r] = 0.0;
+
+  for (int64_t p0 = p_begin; p0 < p_end; p0 += kBN) {
+    __syncthreads();
+    if (tid < kBN) {
+      const int64_t pi = p0 + tid;
+      s_h[tid] = pi < p_end ? (T)(0.5 * (norms[pi] - (double)m[pi])) : tinf<T>();
+    }
+    __syncthreads();
+    T acc[8][8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        acc[r][c] = -(s_h[tile_off(tx, c)] + s_b[tile_off(ty, r)]);
+    simt_mainloop<T, false>(sm, cvt, ldc, c0, vt, ld, p0, d_pad, tx, ty, acc);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      T s = T(0);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) s += tmax(acc[r][c], T(0));
+      g[r] += (double)s;
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    double v = g[r];
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int64_t ci = c0 + tile_off(ty, r);
+    if (tx == 0 && ci < l) partial[split * l + ci] = v;
+  }
+}
+
+// K4: partial[s][j] = sum_{i in split s} min(aux_i, min_{e<card_j} d(v_i, S_j[e]))
+// The running per-(set, point) minima live in shared memory (64 per thread,
+// thread-interleaved so the accesses are conflict-free); the GEMM-form
+// distances of element e come from the same register-blocked mainloop as K3.
+template <typename T>
+struct BatchSmem {
+  SimtSmem<T> mm;
+  T best[64][kThreads];
+  T pa[kBN];   // point norms of the tile (compute type)
+  T px[kBN];   // point aux distances of the tile
+};
+
+template <int DT>
+__global__ void __launch_bounds__(kThreads, (DT == EXEM_F64 ? 1 : 2))
+    batch_eval_kernel(const typename Traits<DT>::C *__restrict__ vt,
+                      int64_t ld, int64_t n, int d_pad,
+                      const double *__restrict__ norms,
+                      const typename Traits<DT>::C *__restrict__ aux,
+                      const typename Traits<DT>::C *__restrict__ packed,
+                      const double *__restrict__ pnorms,
+                      const int32_t *__restrict__ card, int64_t l,
+                      int64_t l_pad, int k_max, int64_t split_pts,
+                      double *__restrict__ partial) {
+  using T = typename Traits<DT>::C;
+  constexpr bool kDirect = Traits<DT>::kDirect;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  BatchSmem<T> &sm = *reinterpret_cast<BatchSmem<T> *>(smem_raw);
+  __shared__ int s_kmax;
+  __shared__ int s_card[kBM];
+  const int tid = threadIdx.x;
+  const int tx = tid % 16, ty = tid / 16;
+  const int64_t j0 = (int64_t)blockIdx.x * kBM;
+  const int64_t split = blockIdx.y;
+  const int64_t p_begin = split * split_pts;
+  const int64_t p_end = min(n, p_begin + split_pts);
+  const int64_t ldp = (int64_t)k_max * l_pad;  // stride between dimensions
+
+  if (tid == 0) s_kmax = 0;
+  __syncthreads();
+  if (tid < kBM) {
+    const int cj = (j0 + tid < l) ? card[j0 + tid] : 0;
+    s_card[tid] = cj;
+    atomicMax(&s_kmax, cj);
+  }
+  __syncthreads();
+  const int kt = s_kmax;  // largest cardinality in this set tile
+
+  double g[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) g[r] = 0.0;
+
+  for (int64_t p0 = p_begin; p0 < p_end; p0 += kBN) {
+    __syncthreads();
+    if (tid < kBN) {
+      const int64_t pi = p0 + tid;
+      sm.pa[tid] = pi < p_end ? (T)norms[pi] : T(0);
+      sm.px[tid] = pi < p_end ? aux[pi] : T(0);
+    }
+#pragma unroll
+    for (int q = 0; q < 64; ++q) sm.best[q][tid] = tinf<T>();
+    for (int e = 0; e < kt; ++e) {
+      T acc[8][8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc[r][c] = T(0);
+      // element e of sets j0..j0+127 at dim k: packed[k*ldp + e*l_pad + j]
+      simt_mainloop<T, kDirect>(sm.mm, packed + (int64_t)e * l_pad, ldp, j0,
+                                vt, ld, p0, d_pad, tx, ty, acc);
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int jr = tile_off(ty, r);
+        if (e < s_card[jr]) {  // blank slots (e >= card) never contribute
+          T be = T(0);
+          if (!kDirect) be = (T)pnorms[(int64_t)e * l_pad + j0 + jr];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            T dist = kDirect ? acc[r][c]
+                             : gemm_form<T>(acc[r][c], sm.pa[tile_off(tx, c)], be);
+            sm.best[r * 8 + c][tid] = tmin(sm.best[r * 8 + c][tid], dist);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      T s = T(0);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const int pc = tile_off(tx, c);
+        if (p0 + pc < p_end) s += tmin(sm.best[r * 8 + c][tid], sm.px[pc]);
+      }
+      g[r] += (double)s;
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    double v = g[r];
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int64_t j = j0 + tile_off(ty, r);
+    if (tx == 0 && j < l) partial[split * l + j] = v;
+  }
+}
+
+// ============================================================ K6 reduce
+__global__ void reduce_partials_kernel(const double *__restrict__ partial,
+                                       int64_t splits, int64_t l,
+                                       double scale, double *__restrict__ out) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= l) return;
+  double s = 0.0;
+  for (int64_t q = 0; q < splits; ++q) s += partial[q * l + j];
+  out[j] = scale * s;
+}
+
+// ============================================================ K5 argmax
+struct Best {
+  double v;
+  int64_t i;
+};
+__device__ __forceinline__ Best better(Best a, Best b) {
+  // larger value wins; equal values -> lower index (np.argmax, optimize.py:73)
+  if (b.v > a.v || (b.v == a.v && b.i < a.i)) return b;
+  return a;
+}
+__device__ __forceinline__ Best warp_best(Best x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    Best y;
+    y.v = __shfl_xor_sync(0xffffffffu, x.v, o);
+    y.i = __shfl_xor_sync(0xffffffffu, x.i, o);
+    x = better(x, y);
+  }
+  return x;
+}
+constexpr int kArgThreads = 1024;
+__device__ __forceinline__ Best block_best(Best x) {
+  __shared__ double sv[32];
+  __shared__ long long si[32];
+  x = warp_best(x);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    sv[w] = x.v;
+    si[w] = x.i;
+  }
+  __syncthreads();
+  Best r{-tinf<double>(), INT64_MAX};
+  if (w == 0) {
+    if (lane < (int)(blockDim.x >> 5)) r = Best{sv[lane], (int64_t)si[lane]};
+    r = warp_best(r);
+  }
+  return r;
+}
+
+__global__ void __launch_bounds__(kArgThreads)
+    argmax_partial_kernel(const double *__restrict__ g, int64_t l,
+                          const uint8_t *__restrict__ selected,
+                          double *__restrict__ scratch) {
+  Best x{-tinf<double>(), INT64_MAX};
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < l;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    double v = g[j];
+    if (!selected[j] && !(v != v)) x = better(x, Best{v, j});
+  }
+  x = block_best(x);
+  if (threadIdx.x == 0) {
+    scratch[2 * blockIdx.x] = x.v;
+    scratch[2 * blockIdx.x + 1] = __longlong_as_double((long long)x.i);
+  }
+}
+
+__global__ void __launch_bounds__(kArgThreads)
+    argmax_final_kernel(const double *__restrict__ scratch, int nblocks,
+                        uint8_t *__restrict__ selected,
+                        const int64_t *__restrict__ index_map, int64_t step,
+                        int64_t *__restrict__ sel_idx,
+                        double *__restrict__ sel_gain) {
+  Best x{-tinf<double>(), INT64_MAX};
+  for (int b = threadIdx.x; b < nblocks; b += blockDim.x)
+    x = better(x, Best{scratch[2 * b],
+                       (int64_t)__double_as_longlong(scratch[2 * b + 1])});
+  x = block_best(x);
+  if (threadIdx.x == 0) {
+    int64_t j = x.i;
+    if (j == INT64_MAX) j = 0;  // unreachable for k <= n (optimize.py:47-50)
+    selected[j] = 1;
+    sel_idx[step] = index_map ? index_map[j] : j;
+    sel_gain[step] = x.v;
+  }
+}
+
+// ============================================================ distances
+template <int DT>
+__global__ void distance_matrix_kernel(const typename Traits<DT>::C *a,
+                                       const double *an, int64_t m,
+                                       const typename Traits<DT>::C *b,
+                                       const double *bn, int64_t q, int d,
+                                       int64_t d_pad,
+                                       typename Traits<DT>::C *out) {
+  using C = typename Traits<DT>::C;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= m * q) return;
+  const int64_t i = idx / q, j = idx % q;
+  C acc = C(0);
+  for (int k = 0; k < d; ++k) {
+    const C x = a[i * d_pad + k], y = b[j * d_pad + k];
+    if (Traits<DT>::kDirect) {
+      const C df = x - y;
+      acc = fma(df, df, acc);
+    } else {
+      acc = fma(x, y, acc);
+    }
+  }
+  out[idx] = Traits<DT>::kDirect ? acc : gemm_form<C>(acc, (C)an[i], (C)bn[j]);
+}
+
+template <typename C>
+__global__ void row_norms_kernel(const C *x, int64_t rows, int d,
+                                 int64_t d_pad, double *out) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  double s = 0.0;
+  for (int k = 0; k < d; ++k) {
+    double v = (double)x[r * d_pad + k];
+    s += v * v;
+  }
+  out[r] = s;
+}
+
+// pnorms[e][j] = ||S_j[e]||^2 from the packed dim-major layout
+// (coalesced over j).
+template <typename C>
+__global__ void packed_norms_kernel(const C *__restrict__ packed, int d,
+                                    int64_t k_max, int64_t l_pad,
+                                    double *__restrict__ out) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t total = k_max * l_pad;
+  if (idx >= total) return;
+  double s = 0.0;
+  for (int k = 0; k < d; ++k) {
+    const double v = (double)packed[(int64_t)k * total + idx];
+    s += v * v;
+  }
+  out[idx] = s;
+}
+
+}  // namespace exem
+
+using namespace exem;
+
+// ============================================================ C-ABI
+extern "C" {
+
+const char *exem_last_error(void) { return g_err; }
+int exem_abi_version(void) { return 1; }
+int64_t exem_launch_count(void) {
+  return (int64_t)__atomic_load_n(&g_launches, __ATOMIC_RELAXED);
+}
+
+int exem_device_info(int device, int *sm_count, int *cc_major, int *cc_minor,
+                     int64_t *smem_optin) {
+  cudaDeviceProp p;
+  cudaError_t e = cudaGetDeviceProperties(&p, device);
+  if (e != cudaSuccess)
+    return fail(EXEM_ERR_UNSUPPORTED, "cudaGetDeviceProperties: %s",
+                cudaGetErrorString(e));
+  if (sm_count) *sm_count = p.multiProcessorCount;
+  if (cc_major) *cc_major = p.major;
+  if (cc_minor) *cc_minor = p.minor;
+  if (smem_optin) *smem_optin = (int64_t)p.sharedMemPerBlockOptin;
+  return EXEM_OK;
+}
+
+int64_t exem_pad_points(int64_t n) {
+  return round_up(n < 1 ? 1 : n, kPointPad);
+}
+int64_t exem_pad_dims(int64_t d) { return round_up(d < 1 ? 1 : d, kDimPad); }
+int64_t exem_split_points(int64_t n) {
+  // A function of n only, so per-set sums never depend on l, chunking or the
+  // number of ranks (cf. fixed COL_BLOCK, core.py:27-30).  Multiple of 256.
+  int64_t target = n / 16;
+  int64_t p = 1024;
+  while (p * 2 <= target && p < 32768) p *= 2;
+  return p;
+}
+int64_t exem_num_splits(int64_t n) {
+  return ceil_div(n < 1 ? 1 : n, exem_split_points(n));
+}
+int64_t exem_tc_kp(int64_t d) { return round_up(d + kTcConst, kTcKChunk); }
+int64_t exem_tc_rows(int64_t n) { return round_up(n < 1 ? 1 : n, kPointPad); }
+int64_t exem_reduce_scratch(int64_t count) {
+  int64_t b = ceil_div(count < 1 ? 1 : count, kRedThreads);
+  return b < 2 * 1024 ? 2 * 1024 : b;  // also covers argmax's 2*blocks
+}
+
+int exem_ground_prepare(int dtype, const void *src, int64_t n, int64_t d,
+                        const void *e0, void *vt, int64_t ld, double *norms,
+                        void *aux, double *aux_sum, double *scratch,
+                        void *stream) {
+  if (n < 1 || d < 1 || ld < n || ld % kPointPad)
+    return fail(EXEM_ERR_ARG, "ground_prepare: bad shape n=%lld d=%lld ld=%lld",
+                (long long)n, (long long)d, (long long)ld);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int d_pad = (int)exem_pad_dims(d);
+  const int64_t blocks = ceil_div(ld, kRedThreads);
+  EXEM_DISPATCH(dtype, DT, {
+    using S = typename Traits<DT>::S;
+    using C = typename Traits<DT>::C;
+    ground_prepare_kernel<DT><<<(unsigned)blocks, kRedThreads, 0, st>>>(
+        (const S *)src, n, (int)d, d_pad, (const S *)e0, (C *)vt, ld, norms,
+        (C *)aux, scratch);
+    EXEM_LAUNCH_CHECK("ground_prepare_kernel");
+  });
+  return reduce_fixed(scratch, blocks, aux_sum, 0, st);
+}
+
+int exem_set_min(int dtype, const void *vt, int64_t ld, int64_t n, int64_t d,
+                 const double *norms, const void *aux, const void *elems,
+                 const double *enorms, int64_t k, int include_aux, void *t_out,
+                 int64_t *label_out, double *sum_out, double *scratch,
+                 void *stream) {
+  if (n < 1 || d < 1 || k < 0)
+    return fail(EXEM_ERR_ARG, "set_min: bad shape");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int d_pad = (int)exem_pad_dims(d);
+  const int64_t blocks = ceil_div(n, kRedThreads);
+  EXEM_DISPATCH(dtype, DT, {
+    using C = typename Traits<DT>::C;
+    size_t smem = (size_t)kSetChunk * d_pad * sizeof(C);
+    if (smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(
+          set_min_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+          (int)smem);
+      if (e != cudaSuccess)
+        return fail(EXEM_ERR_CUDA, "set_min smem: %s", cudaGetErrorString(e));
+    }
+    set_min_kernel<DT><<<(unsigned)blocks, kRedThreads, smem, st>>>(
+        (const C *)vt, ld, n, (int)d, norms, (const C *)aux, (const C *)elems,
+        d_pad, enorms, (int)k, include_aux, (C *)t_out, label_out, scratch);
+    EXEM_LAUNCH_CHECK("set_min_kernel");
+  });
+  if (sum_out) return reduce_fixed(scratch, blocks, sum_out, 0, st);
+  return EXEM_OK;
+}
+
+int exem_greedy_init(int dtype, const void *aux, int64_t n, void *m,
+                     double *msum_out, double *scratch, void *stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t blocks = ceil_div(n, kRedThreads);
+  if (dtype == EXEM_F64) {
+    greedy_init_kernel<double><<<(unsigned)blocks, kRedThreads, 0, st>>>(
+        (const double *)aux, n, (double *)m, scratch);
+  } else {
+    greedy_init_kernel<float><<<(unsigned)blocks, kRedThreads, 0, st>>>(
+        (const float *)aux, n, (float *)m, scratch);
+  }
+  EXEM_LAUNCH_CHECK("greedy_init_kernel");
+  return reduce_fixed(scratch, blocks, msum_out, 0, st);
+}
+
+int exem_greedy_update(int dtype, const void *vt, int64_t ld, int64_t n,
+                       int64_t d, const double *norms, const void *cvt,
+                       int64_t ldc, const double *cnorms,
+                       const int64_t *sel_idx, int64_t step, void *m,
+                       void *xp, int64_t kp, double *msum, double *scratch,
+                       void *stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t blocks = ceil_div(n, kRedThreads);
+  EXEM_DISPATCH(dtype, DT, {
+    using S = typename Traits<DT>::S;
+    using C = typename Traits<DT>::C;
+    greedy_update_kernel<DT><<<(unsigned)blocks, kRedThreads, 0, st>>>(
+        (const C *)vt, ld, n, (int)d, norms, (const C *)cvt, ldc, cnorms,
+        sel_idx, step, (C *)m, (S *)xp, kp, scratch);
+    EXEM_LAUNCH_CHECK("greedy_update_kernel");
+  });
+  return reduce_fixed(scratch, blocks, msum, step, st);
+}
+
+static int simt_grid_ok(int64_t rows, int64_t n, int64_t split_pts,
+                        int64_t splits) {
+  if (split_pts < kBN || split_pts % kBN)
+    return fail(EXEM_ERR_ARG, "split_pts must be a positive multiple of %d",
+                kBN);
+  if (splits != ceil_div(n, split_pts))
+    return fail(EXEM_ERR_ARG, "splits=%lld != ceil(n/split_pts)=%lld",
+                (long long)splits, (long long)ceil_div(n, split_pts));
+  if (ceil_div(rows, kBM) > 0x7fffffffll || splits > 65535)
+    return fail(EXEM_ERR_ARG, "grid too large");
+  return EXEM_OK;
+}
+
+int exem_greedy_gains_simt(int dtype, const void *cvt, int64_t ldc,
+                           const double *cnorms, int64_t l, const void *vt,
+                           int64_t ld, const double *norms, const void *m,
+                           int64_t n, int64_t d, int64_t split_pts,
+                           double *partial, int64_t splits, void *stream) {
+  if (int rc = simt_grid_ok(l, n, split_pts, splits)) return rc;
+  if (ldc % kBM || ld % kBN || ldc < round_up(l, kBM))
+    return fail(EXEM_ERR_ARG, "greedy_gains_simt: leading dims not padded");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int d_pad = (int)exem_pad_dims(d);
+  dim3 grid((unsigned)ceil_div(l, kBM), (unsigned)splits);
+  if (dtype == EXEM_F32) {
+    size_t smem = sizeof(SimtSmem<float>);
+    gains_simt_kernel<float, 2><<<grid, kThreads, smem, st>>>(
+        (const float *)cvt, ldc, cnorms, l, (const float *)vt, ld, norms,
+        (const float *)m, n, d_pad, split_pts, partial);
+    EXEM_LAUNCH_CHECK("gains_simt_kernel<f32>");
+  } else if (dtype == EXEM_F64) {
+    size_t smem = sizeof(SimtSmem<double>);
+    gains_simt_kernel<double, 1><<<grid, kThreads, smem, st>>>(
+        (const double *)cvt, ldc, cnorms, l, (const double *)vt, ld, norms,
+        (const double *)m, n, d_pad, split_pts, partial);
+    EXEM_LAUNCH_CHECK("gains_simt_kernel<f64>");
+  } else {
+    return fail(EXEM_ERR_ARG,
+                "greedy_gains_simt handles f32/f64; half precisions use the "
+                "tcgen05 path (exem_greedy_gains_tc)");
+  }
+  return EXEM_OK;
+}
+
+int exem_batch_eval(int dtype, const void *vt, int64_t ld, int64_t n,
+                    int64_t d, const double *norms, const void *aux,
+                    const void *packed, const double *pnorms,
+                    const int32_t *card, int64_t l, int64_t l_pad,
+                    int64_t k_max, int64_t split_pts, double *partial,
+                    int64_t splits, void *stream) {
+  if (int rc = simt_grid_ok(l, n, split_pts, splits)) return rc;
+  if (l_pad % kBM || l_pad < l || ld % kBN || k_max < 1)
+    return fail(EXEM_ERR_ARG, "batch_eval: bad padding l_pad=%lld",
+                (long long)l_pad);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int d_pad = (int)exem_pad_dims(d);
+  dim3 grid((unsigned)ceil_div(l, kBM), (unsigned)splits);
+  EXEM_DISPATCH(dtype, DT, {
+    using C = typename Traits<DT>::C;
+    size_t smem = sizeof(BatchSmem<C>);
+    cudaError_t e = cudaFuncSetAttribute(
+        batch_eval_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        (int)smem);
+    if (e != cudaSuccess)
+      return fail(EXEM_ERR_CUDA, "batch_eval smem: %s", cudaGetErrorString(e));
+    batch_eval_kernel<DT><<<grid, kThreads, smem, st>>>(
+        (const C *)vt, ld, n, d_pad, norms, (const C *)aux, (const C *)packed,
+        pnorms, card, l, l_pad, (int)k_max, split_pts, partial);
+    EXEM_LAUNCH_CHECK("batch_eval_kernel");
+  });
+  return EXEM_OK;
+}
+
+int exem_reduce_partials(const double *partial, int64_t splits, int64_t l,
+                         double scale, double *out, void *stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  reduce_partials_kernel<<<(unsigned)ceil_div(l, 256), 256, 0, st>>>(
+      partial, splits, l, scale, out);
+  EXEM_LAUNCH_CHECK("reduce_partials_kernel");
+  return EXEM_OK;
+}
+
+int exem_argmax_select(const double *gains, int64_t l, uint8_t *selected,
+                       const int64_t *index_map, int64_t step,
+                       int64_t *sel_idx, double *sel_gain, double *scratch,
+                       void *stream) {
+  if (l < 1) return fail(EXEM_ERR_ARG, "argmax over an empty candidate set");
+  cudaStream_t st = (cudaStream_t)stream;
+  int nb = (int)ceil_div(l, kArgThreads);
+  if (nb > 296) nb = 296;  // 2 waves of 148 SMs; grid-stride inside
+  argmax_partial_kernel<<<nb, kArgThreads, 0, st>>>(gains, l, selected,
+                                                    scratch);
+  EXEM_LAUNCH_CHECK("argmax_partial_kernel");
+  argmax_final_kernel<<<1, kArgThreads, 0, st>>>(scratch, nb, selected,
+                                                 index_map, step, sel_idx,
+                                                 sel_gain);
+  EXEM_LAUNCH_CHECK("argmax_final_kernel");
+  return EXEM_OK;
+}
+
+int exem_distance_matrix(int dtype, const void *a, const double *anorms,
+                         int64_t m, const void *b, const double *bnorms,
+                         int64_t q, int64_t d, int64_t d_pad, void *out,
+                         void *stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t total = m * q;
+  if (total == 0) return EXEM_OK;
+  EXEM_DISPATCH(dtype, DT, {
+    using C = typename Traits<DT>::C;
+    distance_matrix_kernel<DT><<<(unsigned)ceil_div(total, 256), 256, 0, st>>>(
+        (const C *)a, anorms, m, (const C *)b, bnorms, q, (int)d, d_pad,
+        (C *)out);
+    EXEM_LAUNCH_CHECK("distance_matrix_kernel");
+  });
+  return EXEM_OK;
+}
+
+int exem_row_norms(int dtype, const void *x, int64_t rows, int64_t d,
+                   int64_t d_pad, double *out, void *stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (rows == 0) return EXEM_OK;
+  if (dtype == EXEM_F64)
+    row_norms_kernel<double><<<(unsigned)ceil_div(rows, 256), 256, 0, st>>>(
+        (const double *)x, rows, (int)d, d_pad, out);
+  else
+    row_norms_kernel<float><<<(unsigned)ceil_div(rows, 256), 256, 0, st>>>(
+        (const float *)x, rows, (int)d, d_pad, out);
+  EXEM_LAUNCH_CHECK("row_norms_kernel");
+  return EXEM_OK;
+}
+
+int exem_packed_norms(int dtype, const void *packed, int64_t d, int64_t k_max,
+                      int64_t l_pad, double *out, void *stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t total = k_max * l_pad;
+  if (total == 0) return EXEM_OK;
+  const unsigned grid = (unsigned)ceil_div(total, 256);
+  if (dtype == EXEM_F64)
+    packed_norms_kernel<double><<<grid, 256, 0, st>>>((const double *)packed,
+                                                      (int)d, k_max, l_pad, out);
+  else
+    packed_norms_kernel<float><<<grid, 256, 0, st>>>((const float *)packed,
+                                                     (int)d, k_max, l_pad, out);
+  EXEM_LAUNCH_CHECK("packed_norms_kernel");
+  return EXEM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,558 @@
+// exem_tc.cu -- tcgen05 / TMEM / TMA kernel for the optimizer-aware batched
+// Greedy gains (K3-TC), sm_100a only.
+//
+// Replaces the per-step batch of explicit sets S u {c} that greedy_maximize
+// builds and evaluates, pkg/src/exembatch/optimize.py:61-71 (through
+// evaluate.py:142-149 / objective.py:75-90), by one persistent launch that
+// evaluates every candidate of the step:
+//
+//   D[c][i] = x_c . y_i  with  x_c = [c, 1,1,1, -b_hi,-b_mid,-b_lo, 0..]
+//                              y_i = [v_i, -h_hi,-h_mid,-h_lo, 1,1,1, 0..]
+//   b = ||c||^2/2, h_i = (||v_i||^2 - m_i)/2   =>   D = (m_i - d(v_i,c))/2
+//   partial[split][c] = sum_{i in split} max(0, D[c][i])   (x2 in K6)
+//
+// Roles (320 threads, 1 CTA/SM, persistent over (split, candidate tile)):
+//   warp 0      TMA producer: candidate tile (A, stationary per item) and
+//               point tiles (B, streamed per 64-wide K chunk) into 128B-
+//               swizzled smem, mbarrier complete_tx.
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer,
+//               M=128 candidates x N=256 points x K=16, fp32 accum in TMEM,
+//               two accumulator buffers (2 x 256 columns) so the epilogue
+//               of tile t overlaps the MMAs of tile t+1.
+//   warps 2-9   epilogue: tcgen05.ld 32x32b -> relu-sum per candidate row
+//               in registers (fp32 per tile, fp64 across tiles), fixed-order
+//               merge of the two column halves, one store per candidate.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "exem_common.cuh"
+
+namespace exem {
+namespace tc {
+
+constexpr int BM = 128;            // candidates per tile (TMEM lanes)
+constexpr int BN = 256;            // points per tile (TMEM columns)
+constexpr int KCH = 64;            // elements per K chunk (128 B rows)
+constexpr int A_CHUNK = BM * 128;  // bytes of one A K-chunk
+constexpr int B_CHUNK = BN * 128;  // bytes of one B K-chunk
+constexpr int kThreads = 320;
+constexpr int kEpiWarps = 8;
+constexpr int kSmemBudget = 227 * 1024;
+constexpr int kBarBytes = 1024;
+
+__device__ __forceinline__ uint32_t su32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)),
+               "r"(cnt));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t bytes) {
+  asm volatile(
+      "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)),
+      "r"(bytes)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
+  const uint32_t a = su32(b);
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map,
+                                            uint64_t *bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::"
+      "bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(su32(dst)),
+      "l"((uint64_t)map), "r"(x), "r"(y), "r"(su32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t *bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 "
+      "[%0];" ::"r"(su32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t adesc,
+                                         uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(
+          tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+// K-major, 128B-swizzled smem operand descriptor (tcgen05 "version 1").
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;                 // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;       // SBO: 8 rows x 128 B
+  d |= (uint64_t)1 << 46;                 // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;                 // SWIZZLE_128B
+  return d;
+}
+// Instruction descriptor: kind::f16, fp32 accumulate, K-major A and B.
+__host__ __device__ constexpr uint32_t make_idesc(bool bf16, int m, int n) {
+  return (1u << 4)                      // D format F32
+         | ((bf16 ? 1u : 0u) << 7)      // A format
+         | ((bf16 ? 1u : 0u) << 10)     // B format
+         | ((uint32_t)(n >> 3) << 17)   // N >> 3
+         | ((uint32_t)(m >> 4) << 24);  // M >> 4
+}
+
+#define TMEM_LD32(taddr, r)                                                   \
+  asm volatile(                                                               \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "                               \
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"               \
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, "    \
+      "[%32];"                                                                \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]),           \
+        "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]),           \
+        "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),      \
+        "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),      \
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),      \
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),      \
+        "=r"(r[30]), "=r"(r[31])                                              \
+      : "r"(taddr))
+
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+struct Params {
+  int64_t l;            // candidates
+  int64_t n;            // points of this shard
+  int64_t split_pts;    // points per split (multiple of BN)
+  int64_t splits;
+  int64_t cand_tiles;
+  int ksteps;           // K=16 MMA steps  (ceil((d+6)/16))
+  int kchunks;          // 64-wide K chunks loaded per operand tile
+  int stages;           // B pipeline depth (in K chunks)
+  uint32_t idesc;
+  double *partial;
+};
+
+template <bool kAStream>
+__global__ void __launch_bounds__(kThreads, 1)
+    gains_tc_kernel(const __grid_constant__ CUtensorMap map_c,
+                    const __grid_constant__ CUtensorMap map_p,
+                    const Params p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // 1024-align the dynamic smem base (swizzle atoms).
+  unsigned char *smem = (unsigned char *)(((uintptr_t)smem_raw + 1023) &
+                                          ~(uintptr_t)1023);
+  const int a_bytes = kAStream ? 0 : p.kchunks * A_CHUNK;
+  const int stage_bytes = B_CHUNK + (kAStream ? A_CHUNK : 0);
+  unsigned char *sa = smem;                      // stationary A chunks
+  unsigned char *sb = smem + a_bytes;            // stages
+  uint64_t *bars = (uint64_t *)(sb + p.stages * stage_bytes);
+  uint64_t *full = bars;                         // [stages]
+  uint64_t *empty = bars + p.stages;             // [stages]
+  uint64_t *tfull = bars + 2 * p.stages;         // [2]
+  uint64_t *tempty = tfull + 2;                  // [2]
+  uint64_t *afull = tempty + 2;                  // [1]
+  uint64_t *aempty = afull + 1;                  // [1]
+  uint32_t *tmem_slot = (uint32_t *)(aempty + 1);
+  double *red = (double *)(tmem_slot + 4);       // [BM] half-merge buffer
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], kEpiWarps);
+    }
+    mbar_init(afull, 1);
+    mbar_init(aempty, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&map_c));
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&map_p));
+  }
+  if (warp == 1) {
+    asm volatile(
+        "tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::
+            "r"(su32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const int64_t items = p.cand_tiles * p.splits;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t ph = 0, aph = 0;
+      for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+        const int64_t ct = it % p.cand_tiles, sp = it / p.cand_tiles;
+        const int crow = (int)(ct * BM);
+        if (!kAStream) {
+          mbar_wait(aempty, aph ^ 1);
+          aph ^= 1;
+          mbar_expect_tx(afull, (uint32_t)(p.kchunks * A_CHUNK));
+          for (int kc = 0; kc < p.kchunks; ++kc)
+            tma_load_2d(sa + kc * A_CHUNK, &map_c, afull, kc * KCH, crow);
+        }
+        const int64_t p0 = sp * p.split_pts;
+        const int64_t p1 = min(p.n, p0 + p.split_pts);
+        for (int64_t pt = p0; pt < p1; pt += BN) {
+          for (int kc = 0; kc < p.kchunks; ++kc) {
+            mbar_wait(&empty[stage], ph ^ 1);
+            unsigned char *dst = sb + stage * stage_bytes;
+            mbar_expect_tx(&full[stage], (uint32_t)stage_bytes);
+            tma_load_2d(dst, &map_p, &full[stage], kc * KCH, (int)pt);
+            if (kAStream)
+              tma_load_2d(dst + B_CHUNK, &map_c, &full[stage], kc * KCH, crow);
+            if (++stage == p.stages) {
+              stage = 0;
+              ph ^= 1;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    int stage = 0, buf = 0;
+    uint32_t ph = 0, aph = 0;
+    uint32_t tph[2] = {0, 0};
+    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+      const int64_t sp = it / p.cand_tiles;
+      if (!kAStream) {
+        mbar_wait(afull, aph);
+        aph ^= 1;
+        fence_after();
+      }
+      const int64_t p0 = sp * p.split_pts;
+      const int64_t p1 = min(p.n, p0 + p.split_pts);
+      for (int64_t pt = p0; pt < p1; pt += BN) {
+        mbar_wait(&tempty[buf], tph[buf] ^ 1);
+        tph[buf] ^= 1;
+        fence_after();
+        const uint32_t dcol = tmem + (uint32_t)(buf * BN);
+        for (int kc = 0; kc < p.kchunks; ++kc) {
+          mbar_wait(&full[stage], ph);
+          fence_after();
+          unsigned char *bsm = sb + stage * stage_bytes;
+          const uint32_t abase =
+              kAStream ? su32(bsm + B_CHUNK) : su32(sa + kc * A_CHUNK);
+          const uint32_t bbase = su32(bsm);
+          const int k_lo = kc * (KCH / 16);
+          const int k_hi = min(p.ksteps, k_lo + KCH / 16);
+          if (lane == 0) {
+            for (int ks = k_lo; ks < k_hi; ++ks) {
+              const uint32_t off = (uint32_t)((ks - k_lo) * 32);
+              umma_f16(dcol, sw128_desc(abase + off), sw128_desc(bbase + off),
+                       p.idesc, (ks > 0) ? 1u : 0u);
+            }
+            umma_commit(&empty[stage]);
+          }
+          __syncwarp();
+          if (++stage == p.stages) {
+            stage = 0;
+            ph ^= 1;
+          }
+        }
+        if (lane == 0) umma_commit(&tfull[buf]);
+        __syncwarp();
+        buf ^= 1;
+      }
+      if (!kAStream) {
+        if (lane == 0) umma_commit(aempty);
+        __syncwarp();
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int ew = warp - 2;            // 0..7
+    const int q = warp & 3;             // TMEM lane quarter of this warp
+    const int half = ew >> 2;           // column half of the 256-wide tile
+    const int row = q * 32 + lane;      // candidate row within the tile
+    int buf = 0;
+    uint32_t tph[2] = {0, 0};
+    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+      const int64_t ct = it % p.cand_tiles, sp = it / p.cand_tiles;
+      const int64_t p0 = sp * p.split_pts;
+      const int64_t p1 = min(p.n, p0 + p.split_pts);
+      double g = 0.0;
+      for (int64_t pt = p0; pt < p1; pt += BN) {
+        mbar_wait(&tfull[buf], tph[buf]);
+        tph[buf] ^= 1;
+        fence_after();
+        const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) +
+                               (uint32_t)(buf * BN + half * 128);
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          uint32_t r0[32], r1[32];
+          TMEM_LD32(taddr + h2 * 64, r0);
+          TMEM_LD32(taddr + h2 * 64 + 32, r1);
+          tmem_wait_ld();
+          if (h2 == 1) {
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[buf]);
+          }
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            s0 += fmaxf(__uint_as_float(r0[j]), 0.f);
+            s1 += fmaxf(__uint_as_float(r0[j + 1]), 0.f);
+            s2 += fmaxf(__uint_as_float(r0[j + 2]), 0.f);
+            s3 += fmaxf(__uint_as_float(r0[j + 3]), 0.f);
+          }
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            s0 += fmaxf(__uint_as_float(r1[j]), 0.f);
+            s1 += fmaxf(__uint_as_float(r1[j + 1]), 0.f);
+            s2 += fmaxf(__uint_as_float(r1[j + 2]), 0.f);
+            s3 += fmaxf(__uint_as_float(r1[j + 3]), 0.f);
+          }
+        }
+        g += (double)((s0 + s1) + (s2 + s3));
+        buf ^= 1;
+      }
+      // fixed-order merge of the two column halves
+      if (half == 1) red[row] = g;
+      asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+      if (half == 0) {
+        const double tot = g + red[row];
+        const int64_t c = ct * BM + row;
+        if (c < p.l) p.partial[sp * p.l + c] = tot;
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+    }
+  }
+
+  fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    fence_after();
+    asm volatile(
+        "tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// ---------------------------------------------------------------- packing
+// Transposes the SIMT layout vt[d_pad][ld] into point-major half rows and
+// appends the folded constant columns (see header comment).
+template <int DT, bool kCand>
+__global__ void pack_kernel(const float *__restrict__ vt, int64_t ld,
+                            int64_t n, int d, const double *__restrict__ norms,
+                            const float *__restrict__ m,
+                            typename Traits<DT>::S *__restrict__ x, int64_t kp,
+                            int64_t rows) {
+  using S = typename Traits<DT>::S;
+  __shared__ float tile[32][33];
+  const int64_t r0 = (int64_t)blockIdx.x * 32;
+  const int k0 = blockIdx.y * 32;
+  // load vt[k0+ty][r0+tx] (coalesced along points)
+  for (int ty = threadIdx.y; ty < 32; ty += blockDim.y) {
+    const int k = k0 + ty;
+    const int64_t r = r0 + threadIdx.x;
+    tile[ty][threadIdx.x] = (k < d && r < n) ? vt[(int64_t)k * ld + r] : 0.f;
+  }
+  __syncthreads();
+  for (int ty = threadIdx.y; ty < 32; ty += blockDim.y) {
+    const int64_t r = r0 + ty;
+    const int k = k0 + threadIdx.x;
+    if (r >= rows || k >= kp) continue;
+    double v = 0.0;
+    if (r < n) {
+      if (k < d) {
+        v = (double)tile[threadIdx.x][ty];
+      } else if (k < d + kTcConst) {
+        const int c = k - d;
+        const bool ones = kCand ? (c < 3) : (c >= 3);
+        if (ones) {
+          v = 1.0;
+        } else {
+          const double t = kCand ? 0.5 * norms[r]
+                                 : 0.5 * (norms[r] - (double)m[r]);
+          const double t0 = (double)to_c(from_d<S>(t));
+          const double t1 = (double)to_c(from_d<S>(t - t0));
+          const double t2 = (double)to_c(from_d<S>(t - t0 - t1));
+          const int piece = kCand ? c - 3 : c;
+          v = -(piece == 0 ? t0 : (piece == 1 ? t1 : t2));
+        }
+      }
+    }
+    x[r * kp + k] = from_d<S>(v);
+  }
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void *p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p,
+                                cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+  }
+  return fn;
+}
+
+static int make_map(CUtensorMap *map, const void *base, int dtype,
+                    int64_t rows, int64_t kp, int box_rows) {
+  auto enc = get_encode();
+  if (!enc) return fail(EXEM_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled missing");
+  cuuint64_t gdim[2] = {(cuuint64_t)kp, (cuuint64_t)rows};
+  cuuint64_t gstride[1] = {(cuuint64_t)(kp * 2)};
+  cuuint32_t box[2] = {(cuuint32_t)KCH, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map,
+                   dtype == EXEM_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                      : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                   2, const_cast<void *>(base), gdim, gstride, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(EXEM_ERR_ARG, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return EXEM_OK;
+}
+
+}  // namespace tc
+}  // namespace exem
+
+using namespace exem;
+
+extern "C" {
+
+int exem_tc_pack_candidates(int dtype, const void *vt, int64_t ld, int64_t n,
+                            int64_t d, const double *norms, void *xc,
+                            void *stream) {
+  if (dtype != EXEM_BF16 && dtype != EXEM_F16)
+    return fail(EXEM_ERR_ARG, "TC operands are bf16/f16 only");
+  const int64_t kp = exem_tc_kp(d), rows = exem_tc_rows(n);
+  dim3 grid((unsigned)ceil_div(rows, 32), (unsigned)ceil_div(kp, 32));
+  dim3 block(32, 8);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == EXEM_BF16)
+    tc::pack_kernel<EXEM_BF16, true><<<grid, block, 0, st>>>(
+        (const float *)vt, ld, n, (int)d, norms, nullptr,
+        (__nv_bfloat16 *)xc, kp, rows);
+  else
+    tc::pack_kernel<EXEM_F16, true><<<grid, block, 0, st>>>(
+        (const float *)vt, ld, n, (int)d, norms, nullptr, (__half *)xc, kp,
+        rows);
+  EXEM_LAUNCH_CHECK("tc_pack_candidates");
+  return EXEM_OK;
+}
+
+int exem_tc_pack_points(int dtype, const void *vt, int64_t ld, int64_t n,
+                        int64_t d, const double *norms, const void *m,
+                        void *xp, void *stream) {
+  if (dtype != EXEM_BF16 && dtype != EXEM_F16)
+    return fail(EXEM_ERR_ARG, "TC operands are bf16/f16 only");
+  const int64_t kp = exem_tc_kp(d), rows = exem_tc_rows(n);
+  dim3 grid((unsigned)ceil_div(rows, 32), (unsigned)ceil_div(kp, 32));
+  dim3 block(32, 8);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == EXEM_BF16)
+    tc::pack_kernel<EXEM_BF16, false><<<grid, block, 0, st>>>(
+        (const float *)vt, ld, n, (int)d, norms, (const float *)m,
+        (__nv_bfloat16 *)xp, kp, rows);
+  else
+    tc::pack_kernel<EXEM_F16, false><<<grid, block, 0, st>>>(
+        (const float *)vt, ld, n, (int)d, norms, (const float *)m,
+        (__half *)xp, kp, rows);
+  EXEM_LAUNCH_CHECK("tc_pack_points");
+  return EXEM_OK;
+}
+
+int exem_greedy_gains_tc(int dtype, const void *xc, int64_t l, const void *xp,
+                         int64_t n, int64_t d, int64_t split_pts,
+                         double *partial, int64_t splits, void *stream) {
+  using namespace exem::tc;
+  if (dtype != EXEM_BF16 && dtype != EXEM_F16)
+    return fail(EXEM_ERR_ARG, "greedy_gains_tc is bf16/f16 only");
+  if (split_pts < BN || split_pts % BN)
+    return fail(EXEM_ERR_ARG, "split_pts must be a multiple of %d", BN);
+  if (splits != ceil_div(n, split_pts))
+    return fail(EXEM_ERR_ARG, "splits mismatch");
+  int dev = 0, sms = 0, major = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  if (major != 10)
+    return fail(EXEM_ERR_UNSUPPORTED,
+                "tcgen05 path needs an sm_100 (B200) device, found sm_%d",
+                major * 10);
+  const int64_t kp = exem_tc_kp(d);
+  const int kchunks = (int)(kp / KCH);
+  const int ksteps = (int)ceil_div(d + kTcConst, 16);
+  Params prm;
+  prm.l = l;
+  prm.n = n;
+  prm.split_pts = split_pts;
+  prm.splits = splits;
+  prm.cand_tiles = ceil_div(l, BM);
+  prm.ksteps = ksteps;
+  prm.kchunks = kchunks;
+  prm.idesc = make_idesc(dtype == EXEM_BF16, BM, BN);
+  prm.partial = partial;
+  // A stationary when it leaves room for >= 3 B chunk stages.
+  const int avail = kSmemBudget - kBarBytes - 1024;
+  const bool astream = (avail - kchunks * A_CHUNK) / B_CHUNK < 3;
+  const int stage_bytes = B_CHUNK + (astream ? A_CHUNK : 0);
+  int stages = (avail - (astream ? 0 : kchunks * A_CHUNK)) / stage_bytes;
+  if (stages > 8) stages = 8;
+  prm.stages = stages;
+  const size_t smem = (size_t)(astream ? 0 : kchunks * A_CHUNK) +
+                      (size_t)stages * stage_bytes + kBarBytes + 1024;
+  CUtensorMap mc, mp;
+  if (int rc = make_map(&mc, xc, dtype, exem_tc_rows(l), kp, BM)) return rc;
+  if (int rc = make_map(&mp, xp, dtype, exem_tc_rows(n), kp, BN)) return rc;
+  const int64_t items = prm.cand_tiles * splits;
+  const unsigned grid = (unsigned)(items < sms ? items : sms);
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e;
+  if (astream) {
+    e = cudaFuncSetAttribute(gains_tc_kernel<true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+    if (e != cudaSuccess)
+      return fail(EXEM_ERR_CUDA, "smem attr: %s", cudaGetErrorString(e));
+    gains_tc_kernel<true><<<grid, kThreads, smem, st>>>(mc, mp, prm);
+  } else {
+    e = cudaFuncSetAttribute(gains_tc_kernel<false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+    if (e != cudaSuccess)
+      return fail(EXEM_ERR_CUDA, "smem attr: %s", cudaGetErrorString(e));
+    gains_tc_kernel<false><<<grid, kThreads, smem, st>>>(mc, mp, prm);
+  }
+  EXEM_LAUNCH_CHECK("gains_tc_kernel");
+  return EXEM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,148 @@
+"""HBM-resident state of a ground set and upload helpers.
+
+A ``DeviceGround`` owns (as torch tensors -- torch is only the allocator and
+stream provider) the device layouts described in DESIGN.md:
+
+* ``vt``     [d_pad][ld]   SIMT layout, column-major like the reference's
+                           F-order V (core.py:286), compute type f32/f64.
+* ``norms``  [ld]  f64     ||v_i||^2 of the stored values.
+* ``aux``    [ld]  compute d(v_i, e0) rounded through the storage dtype.
+* ``xc``     [rows][kp]    bf16/f16 tensor-core candidate operand (lazy).
+
+Everything numeric is done by the kernels of ``libexem_b200.so``.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native as N
+from .errors import ExemError
+
+_torch = None
+
+
+def torch():
+    global _torch
+    if _torch is None:
+        import torch as t
+
+        _torch = t
+    return _torch
+
+
+def require_cuda(device=None) -> int:
+    """Index of the sm_100 device to use; raise loudly if there is none."""
+    t = torch()
+    if not t.cuda.is_available():
+        raise ExemError(
+            "no CUDA device is visible: the B200 evaluator has no CPU path")
+    if device is None:
+        idx = t.cuda.current_device()
+    elif isinstance(device, int):
+        idx = device
+    else:
+        dv = t.device(device)
+        idx = dv.index if dv.index is not None else t.cuda.current_device()
+    major, minor = t.cuda.get_device_capability(idx)
+    if major != 10:
+        raise ExemError(
+            f"device {idx} is sm_{major}{minor}; libexem_b200 is built for "
+            "sm_100a (B200) only")
+    N.lib()  # load the native library now so a missing build fails here
+    return idx
+
+
+def compute_torch_dtype(precision):
+    t = torch()
+    return t.float64 if precision.compute_dtype == np.float64 else t.float32
+
+
+def to_device_bytes(arr: np.ndarray, dev):
+    """Upload a numpy array's raw bytes (any dtype, incl. bf16) to ``dev``."""
+    t = torch()
+    raw = np.ascontiguousarray(arr).reshape(-1).view(np.uint8)
+    host = t.from_numpy(raw.copy() if not raw.flags.writeable else raw)
+    return host.to(dev, non_blocking=False)
+
+
+def padded_rows(rows: np.ndarray, d_pad: int, precision, dev):
+    """[k][d_pad] compute-type device matrix from (k, d) storage values."""
+    t = torch()
+    k, d = rows.shape
+    host = np.zeros((k, d_pad), dtype=precision.compute_dtype)
+    host[:, :d] = np.asarray(rows, dtype=precision.dtype).astype(
+        precision.compute_dtype)
+    return t.from_numpy(host).to(dev)
+
+
+class DeviceGround:
+    """Device layouts of one ground set on one CUDA device."""
+
+    def __init__(self, n, d, precision, device_index):
+        t = torch()
+        lib = N.lib()
+        self.n, self.d, self.precision = int(n), int(d), precision
+        self.device_index = device_index
+        self.dev = t.device("cuda", device_index)
+        self.ld = int(lib.pad_points(self.n))
+        self.d_pad = int(lib.pad_dims(self.d))
+        self.split_pts = int(lib.split_points(self.n))
+        self.splits = int(lib.num_splits(self.n))
+        cdt = compute_torch_dtype(precision)
+        self.vt = t.empty((self.d_pad, self.ld), dtype=cdt, device=self.dev)
+        self.norms = t.empty(self.ld, dtype=t.float64, device=self.dev)
+        self.aux = t.empty(self.ld, dtype=cdt, device=self.dev)
+        self.scratch = t.empty(int(lib.reduce_scratch(self.ld)),
+                               dtype=t.float64, device=self.dev)
+        self.aux_sum = t.empty(1, dtype=t.float64, device=self.dev)
+        self._xc = None
+        self.kp = int(lib.tc_kp(self.d)) if precision.is_half else 0
+
+    @property
+    def stream(self):
+        return N.stream_handle(self.dev)
+
+    def xc(self):
+        """Tensor-core candidate operand [tc_rows][kp] (built once)."""
+        if self._xc is None:
+            t = torch()
+            lib = N.lib()
+            rows = int(lib.tc_rows(self.n))
+            tdt = t.bfloat16 if self.precision.tag == N.BF16 else t.float16
+            self._xc = t.empty((rows, self.kp), dtype=tdt, device=self.dev)
+            lib.tc_pack_candidates(self.precision.tag, N.ptr(self.vt), self.ld,
+                                   self.n, self.d, N.ptr(self.norms),
+                                   N.ptr(self._xc), self.stream)
+        return self._xc
+
+
+def prepare_ground(matrix: np.ndarray, aux_vec: np.ndarray, precision,
+                   device=None):
+    """Run K1 on the uploaded F-order buffer; return (state, aux_dist, sum)."""
+    t = torch()
+    idx = require_cuda(device)
+    lib = N.lib()
+    n, d = matrix.shape
+    with t.cuda.device(idx):
+        dg = DeviceGround(n, d, precision, idx)
+        src = to_device_bytes(matrix.ravel(order="F"), dg.dev)
+        e0 = to_device_bytes(aux_vec, dg.dev)
+        lib.ground_prepare(precision.tag, N.ptr(src), n, d, N.ptr(e0),
+                           N.ptr(dg.vt), dg.ld, N.ptr(dg.norms), N.ptr(dg.aux),
+                           N.ptr(dg.aux_sum), N.ptr(dg.scratch), dg.stream)
+        aux_host = dg.aux[:n].cpu().numpy().astype(precision.dtype)
+        aux_sum = float(dg.aux_sum.item())
+        del src, e0
+    return dg, aux_host, aux_sum
+
+
+def device_ground(ground, device=None) -> DeviceGround:
+    """Cached ``DeviceGround`` of ``ground`` on ``device`` (built on demand)."""
+    idx = require_cuda(device)
+    dg = ground._device.get(idx)
+    if dg is None:
+        dg, _, _ = prepare_ground(ground.matrix, ground.aux, ground.precision,
+                                  idx)
+        ground._device[idx] = dg
+    return dg

@@ -1,0 +1,223 @@
+"""Batch evaluation and memory-budget chunking (mirror of
+``pkg/src/exembatch/evaluate.py``).
+
+The reference dispatches on a backend string to three host implementations
+(evaluate.py:42,282-293).  Here there is exactly one implementation per call:
+the sm_100a kernels.  The reference's backend names are still accepted by
+``Evaluator`` (so callers constructing ``Evaluator("parallel", ...)`` keep
+working) and all of them select that single device path.
+
+Per set j:  f(S_j) = acc(aux_loss) - acc(sum_i t_i(S_j)) / acc(n)
+with t_i = min(aux_i, min_{e} d(v_i, S_j[e])) summed in fp64 in a fixed order
+by kernel K4 (``exem_batch_eval``) + K6 (``exem_reduce_partials``).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _native as N
+from .core import (
+    DeviceLimits,
+    EvaluationBatch,
+    GroundSet,
+    PackedBatch,
+    Precision,
+    compute_kernel_config,
+    pack_batch,
+)
+from .errors import DimensionMismatchError, OutOfMemoryError
+from .objective import (
+    SQUARED_EUCLIDEAN,
+    Dissimilarity,
+    _as_elements,
+    device_set_min,
+    require_device_dissimilarity,
+)
+
+# Accepted backend names.  "b200" is the native name; the reference's names
+# (evaluate.py:42) are aliases of the same single device path.
+BACKENDS = ("b200", "reference", "parallel", "tiled")
+
+
+@dataclass(frozen=True)
+class Evaluator:
+    """Evaluation settings (evaluate.py:50-65) plus the CUDA device.
+
+    ``limits``/``worker_count`` are kept for signature compatibility; the
+    device path's tiling is fixed by the B200 kernels.
+    """
+
+    backend: str = "b200"
+    limits: DeviceLimits = field(default_factory=DeviceLimits)
+    worker_count: int = 1
+    precision: Optional[Precision] = None
+    device: Optional[int] = None
+
+    def __post_init__(self):
+        if self.backend not in BACKENDS:
+            raise ValueError(
+                f"unknown backend {self.backend!r}; expected one of {BACKENDS}")
+        if self.worker_count < 1:
+            raise ValueError("worker_count must be >= 1")
+
+
+@dataclass(frozen=True)
+class ChunkPlan:
+    """Sets-per-chunk under a memory budget (evaluate.py:68-75)."""
+
+    chunk_size: int
+    chunk_count: int
+    per_set_bytes: int
+    free_bytes: int
+
+
+def estimate_set_memory(n: int, k_max: int, d: int, precision: Precision) -> int:
+    """mu_s = (k_max*d + n) * bytes_per_value + 16 (evaluate.py:78-83;
+    PAPER.md:406-409): the packed slice, one work-matrix row and metadata."""
+    if min(n, k_max, d) < 1:
+        raise ValueError("n, k_max and d must all be >= 1")
+    return (k_max * d + n) * precision.bytes_per_value + 16
+
+
+def plan_chunks(free_bytes: int, per_set_bytes: int, l: int) -> ChunkPlan:
+    """chunk_size = min(floor(phi/mu_s), l); OOM when 0 (evaluate.py:86-102)."""
+    if per_set_bytes < 1 or l < 1:
+        raise ValueError("per_set_bytes and l must be >= 1")
+    fit = free_bytes // per_set_bytes
+    if fit == 0:
+        raise OutOfMemoryError(
+            f"a single evaluation set needs {per_set_bytes} bytes but only "
+            f"{free_bytes} are free; use a lower precision or a larger budget")
+    size = min(fit, l)
+    return ChunkPlan(chunk_size=size, chunk_count=math.ceil(l / size),
+                     per_set_bytes=per_set_bytes, free_bytes=free_bytes)
+
+
+def _check_batch(ground: GroundSet, batch: EvaluationBatch) -> None:
+    if batch.d != ground.d:
+        raise DimensionMismatchError(
+            f"batch is {batch.d}-dim but the ground set is {ground.d}-dim")
+
+
+def _effective_precision(evaluator: Evaluator, ground: GroundSet) -> Precision:
+    if evaluator.precision is not None and evaluator.precision is not ground.precision:
+        raise ValueError(
+            "evaluator precision differs from the ground set precision; "
+            "build the ground set at the desired precision")
+    return ground.precision
+
+
+def _finish(ground: GroundSet, sums: np.ndarray) -> np.ndarray:
+    """acc(aux_loss) - acc(sum)/acc(n) per set (evaluate.py:111-112)."""
+    acc = ground.precision.accumulate_dtype
+    return acc.type(ground.aux_loss) - sums.astype(acc) / acc.type(ground.n)
+
+
+def evaluate_single(ground: GroundSet, set_vectors,
+                    dissimilarity: Dissimilarity = SQUARED_EUCLIDEAN) -> float:
+    """f of one set (evaluate.py:115-123) -- kernel K2 + fixed-order sum."""
+    require_device_dissimilarity(dissimilarity)
+    elems = _as_elements(ground, set_vectors)
+    if elems.shape[0] == 0:
+        return 0.0
+    total, _, _ = device_set_min(ground, elems, include_aux=True)
+    return float(_finish(ground, np.array([total]))[0])
+
+
+def device_packed_sums(ground: GroundSet, values: np.ndarray, d: int,
+                       k_max: int, l: int, cardinalities, device=None):
+    """Upload a packed (d, k_max, l) buffer and run K4 + K6.
+
+    Returns the device tensor of per-set fp64 sums sum_i t_i(S_j).
+    """
+    from .device import torch
+
+    t = torch()
+    lib = N.lib()
+    dg = ground.on_device(device)
+    prec = ground.precision
+    l_pad = int(-(-l // 128) * 128)
+    with t.cuda.device(dg.device_index):
+        st = dg.stream
+        host = np.zeros((dg.d_pad, k_max, l_pad), dtype=prec.compute_dtype)
+        host[:d, :, :l] = np.asarray(values, dtype=prec.dtype).reshape(
+            d, k_max, l).astype(prec.compute_dtype)
+        packed = t.from_numpy(host).to(dg.dev)
+        pnorms = t.empty((k_max, l_pad), dtype=t.float64, device=dg.dev)
+        lib.packed_norms(prec.tag, N.ptr(packed), dg.d, k_max, l_pad,
+                         N.ptr(pnorms), st)
+        card = t.tensor(np.asarray(cardinalities, dtype=np.int32),
+                        device=dg.dev)
+        partial = t.empty((dg.splits, l), dtype=t.float64, device=dg.dev)
+        lib.batch_eval(prec.tag, N.ptr(dg.vt), dg.ld, dg.n, dg.d,
+                       N.ptr(dg.norms), N.ptr(dg.aux), N.ptr(packed),
+                       N.ptr(pnorms), N.ptr(card), l, l_pad, k_max,
+                       dg.split_pts, N.ptr(partial), dg.splits, st)
+        sums = t.empty(l, dtype=t.float64, device=dg.dev)
+        lib.reduce_partials(N.ptr(partial), dg.splits, l, 1.0, N.ptr(sums), st)
+    return sums
+
+
+def tiled_evaluate(ground: GroundSet, packed: PackedBatch,
+                   dissimilarity: Dissimilarity = SQUARED_EUCLIDEAN,
+                   limits: Optional[DeviceLimits] = None,
+                   worker_count: int = 1, instrument: bool = False):
+    """Evaluate a packed batch (evaluate.py:197-270) with kernel K4.
+
+    The packed round-robin buffer is consumed in its own layout; blank slots
+    (e >= card_j) never contribute.  With ``instrument=True`` the reference's
+    staging model is reported alongside: under the paper's kernel
+    configuration every ground vector is staged once per block row covering
+    its column, i.e. ``grid_y`` times (core.py:349-377).
+    """
+    require_device_dissimilarity(dissimilarity)
+    limits = limits or DeviceLimits()
+    config = compute_kernel_config(ground.n, packed.l, ground.bytes_per_vector,
+                                   limits)
+    sums = device_packed_sums(ground, packed.values, packed.d, packed.k_max,
+                              packed.l, packed.cardinalities)
+    out = _finish(ground, sums.cpu().numpy())
+    if instrument:
+        loads = np.full(ground.n, config.grid[1], dtype=np.int64)
+        return out, loads
+    return out
+
+
+def evaluate_batch(evaluator: Evaluator, ground: GroundSet,
+                   batch: EvaluationBatch,
+                   dissimilarity: Dissimilarity = SQUARED_EUCLIDEAN) -> np.ndarray:
+    """One value per set (evaluate.py:273-293) -- kernels K4 + K6."""
+    require_device_dissimilarity(dissimilarity)
+    _check_batch(ground, batch)
+    precision = _effective_precision(evaluator, ground)
+    packed = pack_batch(batch, precision)
+    sums = device_packed_sums(ground, packed.values, packed.d, packed.k_max,
+                              packed.l, packed.cardinalities, evaluator.device)
+    return _finish(ground, sums.cpu().numpy())
+
+
+def evaluate_chunked(evaluator: Evaluator, ground: GroundSet,
+                     batch: EvaluationBatch,
+                     dissimilarity: Dissimilarity = SQUARED_EUCLIDEAN,
+                     budget: int = 0) -> np.ndarray:
+    """Budget-sized chunks of sets, merged in order (evaluate.py:296-319).
+
+    Per-set sums never depend on which other sets share a launch, so the
+    result is bit-identical to ``evaluate_batch``.
+    """
+    _check_batch(ground, batch)
+    precision = _effective_precision(evaluator, ground)
+    mu = estimate_set_memory(ground.n, batch.k_max, batch.d, precision)
+    plan = plan_chunks(budget, mu, batch.l)
+    pieces = []
+    for c in range(plan.chunk_count):
+        lo = c * plan.chunk_size
+        hi = min(lo + plan.chunk_size, batch.l)
+        sub = EvaluationBatch.from_sets(batch.sets[lo:hi])
+        pieces.append(evaluate_batch(evaluator, ground, sub, dissimilarity))
+    return np.concatenate(pieces)
