@@ -1,0 +1,387 @@
+"""Benchmark: BASELINE config 4 -- full Greedy, n=1,000,000, d=100, k=50.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+One "step" is one Greedy iteration over l = n - t candidate sets S u {c}
+(kernel K3 over every candidate, K6 reduce, K5 argmax, K2 m-update).  The
+run is one Greedy of k = W + K steps: the first W steps are untimed warm-up,
+the next K are timed (default 3 + 47 = 50 = BASELINE's k).  N > 1 runs under
+torchrun: V is row-sharded, the l partial gains are all-reduced over NCCL
+each step (strong scaling: the problem is fixed, N GPUs share it).
+
+Prints ONE JSON line on rank 0 (contract in the task statement): value =
+candidate-set evaluations per second for the whole job; ``e2e`` is the same
+metric through the public API (build_ground_set + greedy_maximize from host
+numpy, H2D/D2H inside the timed region); ``roofline`` refers to the dominant
+kernel (gains_tc_kernel, tcgen05); ``cpu_baseline`` times the CPU oracle
+port of the reference's path (oracle/exem_oracle.py) on a bounded sample.
+
+``--impl reference`` times that CPU port alone (all host threads) on the
+same config and prints the same line with "impl": "reference".
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = ("candidate-set evals/sec & dist-evals/s vs roofline "
+          "(n=1M,d=100,k=50) at 1/2/4/8 GPU")
+UNIT = "candidate-set evals/s"
+PRECISION_CHOICES = ("bf16", "fp16", "fp32", "fp64")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=47)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
+    ap.add_argument("--n", type=int, default=1_000_000)
+    ap.add_argument("--d", type=int, default=100)
+    ap.add_argument("--precision", default="bf16", choices=PRECISION_CHOICES)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+def synthetic(n, d, seed):
+    """Gaussian N(0, I) float32; e0 = 0."""
+    return np.random.default_rng(seed).standard_normal((n, d), dtype=np.float32)
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return json.loads(p.read_text()), "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0,
+            "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200",
+                 "-i", str(self.index)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                 "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            parts = [p.strip() for p in ln.split(",")]
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except (ValueError, IndexError):
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [],
+                    "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ CPU leg
+def cpu_sample(n, d, seed, set_size, seconds, threads, V=None):
+    """Time the oracle port of the reference's evaluate path (fp32, parallel
+    row split like evaluate.py:162-170) on sets of ``set_size`` at the
+    full n: returns (sets/s, sets timed)."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import exem_oracle as O  # CPU baseline leg only
+
+    if V is None:
+        V = synthetic(n, d, seed)
+    g = O.Ground(V, np.float32)
+    rng = np.random.default_rng(seed + 1)
+    done, t_total = 0, 0.0
+    while True:  # at least one batch of `threads` sets
+        sets = [g.matrix[np.sort(rng.choice(n, size=set_size, replace=False))]
+                for _ in range(threads)]
+        t0 = time.perf_counter()
+        O.evaluate_batch(g, sets, workers=threads)
+        t_total += time.perf_counter() - t0
+        done += len(sets)
+        if t_total >= seconds:
+            return done / t_total, done, t_total
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU port on the host cores, rank 0 only."""
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    n, d = args.n, args.d
+    V = synthetic(n, d, args.seed)
+    total_sets, total_t = 0, 0.0
+    per_step = max(1.0, min(args.cpu_seconds / 4, 4.0))
+    for step in range(args.warmup, args.warmup + args.steps):
+        set_size = step + 1  # Greedy step t evaluates |S u {c}| = t+1
+        rate, cnt, t = cpu_sample(n, d, args.seed + step, set_size, per_step,
+                                  threads, V)
+        total_sets += cnt
+        total_t += t
+    value = total_sets / total_t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * (n - args.warmup - args.steps / 2) / value,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "fp32", "data": "synthetic Gaussian N(0,1), seed "
+        f"{args.seed}",
+        "config": {"workload": "C4 Greedy n=1M d=100 k=50 (CPU port of the "
+                   "reference, bounded sample per step)", "n": n, "d": d,
+                   "k": args.warmup + args.steps},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads,
+                         "kind": "port",
+                         "sample": f"{total_sets} sets of size t+1 at steps "
+                         f"{args.warmup}..{args.warmup + args.steps - 1}, "
+                         "full n, numpy/OpenBLAS restatement, 1 BLAS thread "
+                         "per worker"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU leg
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    assert args.warmup >= 3, "W >= 3 warm-up steps"
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2101_08763_b200 as pb
+    from paper_2101_08763_b200 import _native as N
+    from paper_2101_08763_b200.distributed import (DeviceShardOps,
+                                                   build_sharded_ground)
+    from paper_2101_08763_b200.optimize import GreedyRun
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    prec = pb.Precision.from_name(args.precision)
+    n, d = args.n, args.d
+    k = args.warmup + args.steps
+    V = synthetic(n, d, args.seed)
+    lib = N.lib()
+
+    sg = build_sharded_ground(V, prec, rank, world, device=local)
+    sp = int(lib.split_points(n))
+    run = GreedyRun(sg.local, cand=sg.cand, k_cap=k, split_pts=sp)
+    ops = DeviceShardOps(run)
+    stream = torch.cuda.current_stream()
+
+    def all_reduce(t):
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # K3 timing: events on the launching (current) stream around each launch
+    ev = []
+    orig = run.compute_gains
+
+    def timed_gains(chunk=None):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        orig(chunk)
+        b.record(stream)
+        ev.append((a, b))
+
+    ops.start()
+    for step in range(args.warmup):
+        ops.local_gains()
+        all_reduce(ops.gains_buffer())
+        ops.select(step)
+        ops.update(step)
+    torch.cuda.synchronize()
+    barrier()
+    run.compute_gains = timed_gains
+    launches0 = lib.launch_count()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        barrier()
+        t0.record(stream)
+        for step in range(args.warmup, k):
+            ops.local_gains()
+            all_reduce(ops.gains_buffer())
+            ops.select(step)
+            ops.update(step)
+        t1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    launches = lib.launch_count() - launches0
+    ms_local = t0.elapsed_time(t1)
+    run.compute_gains = orig
+    all_reduce(ops.msum_buffer())
+    ms_t = torch.tensor([ms_local], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    gains_ms = [a.elapsed_time(b) for a, b in ev]
+    gains_ms_local = float(np.mean(gains_ms))
+
+    picks = run.sel_idx.cpu().numpy()[:k]
+    l_steps = [n - t for t in range(args.warmup, k)]
+    evals = float(sum(l_steps))
+    value = evals / (ms / 1e3)
+    n_local = sg.rows[1] - sg.rows[0]
+
+    # roofline of the dominant kernel: 2*n_local*l*d algorithmic flop/launch
+    peaks, peak_src = load_peaks()
+    half = prec.is_half
+    flop = 2.0 * n_local * float(np.mean(l_steps)) * d
+    achieved = flop / (gains_ms_local / 1e3) / 1e12
+    if half:
+        peak = float(peaks.get("bf16_tflops_sustained",
+                               peaks.get("bf16_tflops")))
+        bound = "tensor"
+    else:
+        peak = float(peaks.get("fp32_ffma_tflops", 74.4)) * (
+            0.5 if prec is pb.Precision.binary64 else 1.0)
+        bound = "fp32-pipe" if prec is pb.Precision.binary32 else "fp64-pipe"
+    traffic = None
+    tfile = ROOT / "profiles" / "gains_tc_traffic.json"
+    if half and tfile.exists():
+        try:
+            traffic = json.loads(tfile.read_text()).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    result = None
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu and world >= 1:
+            threads = os.cpu_count() or 1
+            mid = (args.warmup + k) // 2 + 1
+            rate, cnt, secs = cpu_sample(n, d, args.seed, mid, args.cpu_seconds,
+                                         threads, V)
+            cpu = {"value": rate, "unit": UNIT, "cores": threads,
+                   "kind": "port",
+                   "sample": f"{cnt} sets of size {mid} (mean |S u c| of the "
+                   f"timed steps) at full n={n}, d={d}, fp32, {secs:.1f}s; "
+                   "oracle/exem_oracle.py numpy/OpenBLAS restatement of "
+                   "evaluate.py:142-170"}
+        clocks = clk.summary()
+        result = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step":
+            ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": args.precision,
+            "data": f"synthetic Gaussian N(0,1) float32 seed {args.seed}, "
+                    f"stored as {args.precision}",
+            "config": {"workload": "C4 full Greedy k=50: one step = all l=n-t "
+                       "candidate sets S u {c} (K3 gains + K6 + K5 argmax + "
+                       "K2 m-update)", "n": n, "d": d, "k": k,
+                       "parallelism": f"row-shard x{world}" if world > 1 else
+                       "1 GPU", "l2": "inputs larger than L2 (V operands "
+                       f"{2 * n * 128 * 2 / 2**20:.0f} MiB)"},
+            "dist_evals_per_s": {"executed": n * evals / (ms / 1e3),
+                                 "reference_equivalent": n * sum(
+                                     (n - t) * (t + 1) for t in
+                                     range(args.warmup, k)) / (ms / 1e3)},
+            "roofline": {"bound": bound, "kernel": "gains_tc_kernel" if half
+                         else "gains_simt_kernel", "achieved": achieved,
+                         "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                         "peak_source": f"{peak_src} "
+                         f"{'bf16_tflops_sustained' if half else 'FFMA spec'}",
+                         "traffic": traffic, "algorithmic_flop_per_launch": flop,
+                         "kernel_ms_avg": gains_ms_local,
+                         "kernel_share_of_step": gains_ms_local * args.steps / ms},
+            "cpu_baseline": cpu,
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+            "picks_head": [int(x) for x in picks[:5]],
+        }
+    # ---- e2e through the public API (1 GPU: build_ground_set + greedy)
+    if world == 1 and not args.no_e2e:
+        del run, ops, sg
+        torch.cuda.empty_cache()
+        torch.cuda.synchronize()
+        t_start = time.perf_counter()
+        g = pb.build_ground_set(V, precision=prec)
+        res = pb.greedy_maximize(g, k=k)
+        t_e2e = time.perf_counter() - t_start
+        e2e_evals = float(sum(n - t for t in range(k)))
+        h2d = n * d * prec.bytes_per_value + d * prec.bytes_per_value
+        d2h = n * np.dtype(np.float32).itemsize + 2 * 8 * k + 8
+        result["e2e"] = {"value": e2e_evals / t_e2e, "unit": UNIT,
+                         "h2d_bytes_per_step": h2d / k,
+                         "d2h_bytes_per_step": d2h / k,
+                         "seconds": t_e2e, "steps": k,
+                         "api": "build_ground_set(numpy) + greedy_maximize(k)",
+                         "picks_match_device_run":
+                         list(res.exemplar_indices) == [int(x) for x in picks]}
+    elif rank == 0:
+        result["e2e"] = {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0,
+                         "d2h_bytes_per_step": 0,
+                         "note": "multi-GPU e2e not measured in this round"}
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

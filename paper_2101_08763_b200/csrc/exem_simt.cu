@@ -84,8 +84,10 @@ __global__ void __launch_bounds__(kRedThreads)
         dst += df * df;
       }
     }
-    // aux_distances are stored at the storage dtype (core.py:303-305).
-    C a = (i < n) ? to_c(from_d<S>(dst)) : C(0);
+    // aux_distances are stored at the storage dtype (core.py:303-305);
+    // bfloat16 (not a reference precision) keeps them at binary32.
+    C a = C(0);
+    if (i < n) a = (DT == EXEM_BF16) ? (C)dst : to_c(from_d<S>(dst));
     if (i < n) {
       norms[i] = nrm;
       aux[i] = a;

@@ -53,6 +53,14 @@ def require_cuda(device=None) -> int:
     return idx
 
 
+def aux_dtype(precision) -> np.dtype:
+    """Dtype of GroundSet.aux_distances: the storage dtype like the reference
+    (core.py:303-305), except bfloat16 which keeps binary32."""
+    if precision.tag == N.BF16:
+        return np.dtype(np.float32)
+    return precision.dtype
+
+
 def compute_torch_dtype(precision):
     t = torch()
     return t.float64 if precision.compute_dtype == np.float64 else t.float32
@@ -131,7 +139,7 @@ def prepare_ground(matrix: np.ndarray, aux_vec: np.ndarray, precision,
         lib.ground_prepare(precision.tag, N.ptr(src), n, d, N.ptr(e0),
                            N.ptr(dg.vt), dg.ld, N.ptr(dg.norms), N.ptr(dg.aux),
                            N.ptr(dg.aux_sum), N.ptr(dg.scratch), dg.stream)
-        aux_host = dg.aux[:n].cpu().numpy().astype(precision.dtype)
+        aux_host = dg.aux[:n].cpu().numpy().astype(aux_dtype(precision))
         aux_sum = float(dg.aux_sum.item())
         del src, e0
     return dg, aux_host, aux_sum

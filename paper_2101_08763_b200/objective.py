@@ -205,7 +205,7 @@ def min_distances(ground: GroundSet, elems: np.ndarray,
     if elems.shape[0] == 0:
         t = np.full(ground.n, ground.precision.max_finite, dtype=dtype)
         if include_aux:
-            t = np.minimum(t, ground.aux_distances)
+            t = np.minimum(t, ground.aux_distances).astype(dtype)
         return t
     _, t, _ = device_set_min(ground, elems, include_aux, want_t=True)
     return t.astype(dtype)
