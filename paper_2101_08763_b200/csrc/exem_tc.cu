@@ -23,6 +23,7 @@
 //               in registers (fp32 per tile, fp64 across tiles), fixed-order
 //               merge of the two column halves, one store per candidate.
 #include <cuda.h>
+#include <cstdlib>
 #include <cudaTypedefs.h>
 
 #include "exem_common.cuh"
@@ -39,6 +40,12 @@ constexpr int kThreads = 320;
 constexpr int kEpiWarps = 8;
 constexpr int kSmemBudget = 227 * 1024;
 constexpr int kBarBytes = 1024;
+constexpr int kTrace = 256;  // tiles traced on CTA 0 (EXEM_TC_TRACE)
+#define TR(slot, t)                                                        \
+  do {                                                                     \
+    if (p.trace != nullptr && blockIdx.x == 0 && (t) < kTrace)             \
+      p.trace[(slot) * kTrace + (t)] = clock64();                          \
+  } while (0)
 
 __device__ __forceinline__ uint32_t su32(const void *p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -69,6 +76,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
         : "r"(a), "r"(parity)
         : "memory");
   } while (!ok);
+}
+// Wait with a short back-off between probes: for roles that are not on the
+// tensor-pipe critical path (producer, epilogue), so their polling does not
+// compete with the MMA issuer's own barrier traffic.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *b, uint32_t parity) {
+  const uint32_t a = su32(b);
+  uint32_t ok = 0;
+  while (true) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (ok) return;
+    __nanosleep(64);
+  }
 }
 __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map,
                                             uint64_t *bar, int x, int y) {
@@ -101,6 +126,57 @@ __device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t adesc,
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
       : "memory");
 }
+// NK back-to-back MMAs over one 64-wide K chunk in a single asm block: the
+// descriptors advance by 32 B (2 in the >>4 address field) per K=16 step.
+// kFirst: the first MMA overwrites the accumulator (start of a tile).
+#define EXEM_MMA1(P)                                                         \
+  "tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, " P ";\n\t"
+#define EXEM_STEP "add.s64 a, a, 2;\n\tadd.s64 b, b, 2;\n\t"
+template <int NK, bool kFirst>
+__device__ __forceinline__ void umma_chunk(uint32_t d, uint64_t ad,
+                                           uint64_t bd, uint32_t idesc) {
+  static_assert(NK >= 1 && NK <= 4, "1..4 MMAs per 64-wide chunk");
+  if constexpr (NK == 1)
+    asm volatile("{\n\t.reg .b64 a, b;\n\t.reg .pred pf, pt;\n\t"
+                 "setp.ne.b32 pf, %4, 0;\n\tsetp.eq.b32 pt, 0, 0;\n\t"
+                 "mov.b64 a, %1;\n\tmov.b64 b, %2;\n\t" EXEM_MMA1("pf") "}" ::
+                     "r"(d), "l"(ad), "l"(bd), "r"(idesc), "r"(kFirst ? 0 : 1)
+                 : "memory");
+  if constexpr (NK == 2)
+    asm volatile("{\n\t.reg .b64 a, b;\n\t.reg .pred pf, pt;\n\t"
+                 "setp.ne.b32 pf, %4, 0;\n\tsetp.eq.b32 pt, 0, 0;\n\t"
+                 "mov.b64 a, %1;\n\tmov.b64 b, %2;\n\t" EXEM_MMA1("pf")
+                     EXEM_STEP EXEM_MMA1("pt") "}" ::"r"(d),
+                 "l"(ad), "l"(bd), "r"(idesc), "r"(kFirst ? 0 : 1)
+                 : "memory");
+  if constexpr (NK == 3)
+    asm volatile("{\n\t.reg .b64 a, b;\n\t.reg .pred pf, pt;\n\t"
+                 "setp.ne.b32 pf, %4, 0;\n\tsetp.eq.b32 pt, 0, 0;\n\t"
+                 "mov.b64 a, %1;\n\tmov.b64 b, %2;\n\t" EXEM_MMA1("pf")
+                     EXEM_STEP EXEM_MMA1("pt") EXEM_STEP EXEM_MMA1("pt") "}" ::
+                         "r"(d),
+                 "l"(ad), "l"(bd), "r"(idesc), "r"(kFirst ? 0 : 1)
+                 : "memory");
+  if constexpr (NK == 4)
+    asm volatile("{\n\t.reg .b64 a, b;\n\t.reg .pred pf, pt;\n\t"
+                 "setp.ne.b32 pf, %4, 0;\n\tsetp.eq.b32 pt, 0, 0;\n\t"
+                 "mov.b64 a, %1;\n\tmov.b64 b, %2;\n\t" EXEM_MMA1("pf")
+                     EXEM_STEP EXEM_MMA1("pt") EXEM_STEP EXEM_MMA1("pt")
+                         EXEM_STEP EXEM_MMA1("pt") "}" ::"r"(d),
+                 "l"(ad), "l"(bd), "r"(idesc), "r"(kFirst ? 0 : 1)
+                 : "memory");
+}
+template <bool kFirst>
+__device__ __forceinline__ void umma_chunk_n(int nk, uint32_t d, uint64_t ad,
+                                             uint64_t bd, uint32_t idesc) {
+  switch (nk) {
+    case 1: umma_chunk<1, kFirst>(d, ad, bd, idesc); break;
+    case 2: umma_chunk<2, kFirst>(d, ad, bd, idesc); break;
+    case 3: umma_chunk<3, kFirst>(d, ad, bd, idesc); break;
+    default: umma_chunk<4, kFirst>(d, ad, bd, idesc); break;
+  }
+}
+
 // K-major, 128B-swizzled smem operand descriptor (tcgen05 "version 1").
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   uint64_t d = 0;
@@ -135,6 +211,22 @@ __host__ __device__ constexpr uint32_t make_idesc(bool bf16, int m, int n) {
         "=r"(r[30]), "=r"(r[31])                                              \
       : "r"(taddr))
 
+__device__ __forceinline__ uint32_t and32(const uint32_t (&r)[32]) {
+  uint32_t a = r[0];
+#pragma unroll
+  for (int j = 1; j < 32; ++j) a &= r[j];
+  return a;
+}
+// s_even += max(0, r[2j]), s_odd += max(0, r[2j+1]) in ascending j.
+__device__ __forceinline__ void relu_acc(const uint32_t (&r)[32], float &se,
+                                         float &so) {
+#pragma unroll
+  for (int j = 0; j < 32; j += 2) {
+    se += fmaxf(__uint_as_float(r[j]), 0.f);
+    so += fmaxf(__uint_as_float(r[j + 1]), 0.f);
+  }
+}
+
 __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
@@ -148,8 +240,11 @@ struct Params {
   int ksteps;           // K=16 MMA steps  (ceil((d+6)/16))
   int kchunks;          // 64-wide K chunks loaded per operand tile
   int stages;           // B pipeline depth (in K chunks)
+  int dbg;              // timing experiments only (EXEM_TC_DEBUG), 0 in use
+  int tile_stage;       // 1: a pipeline stage holds a whole B tile
   uint32_t idesc;
   double *partial;
+  long long *trace;     // timing experiments only (EXEM_TC_TRACE)
 };
 
 template <bool kAStream>
@@ -162,7 +257,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   unsigned char *smem = (unsigned char *)(((uintptr_t)smem_raw + 1023) &
                                           ~(uintptr_t)1023);
   const int a_bytes = kAStream ? 0 : p.kchunks * A_CHUNK;
-  const int stage_bytes = B_CHUNK + (kAStream ? A_CHUNK : 0);
+  const int stage_bytes =
+      p.tile_stage ? p.kchunks * B_CHUNK : B_CHUNK + (kAStream ? A_CHUNK : 0);
   unsigned char *sa = smem;                      // stationary A chunks
   unsigned char *sb = smem + a_bytes;            // stages
   uint64_t *bars = (uint64_t *)(sb + p.stages * stage_bytes);
@@ -223,13 +319,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int64_t p0 = sp * p.split_pts;
         const int64_t p1 = min(p.n, p0 + p.split_pts);
         for (int64_t pt = p0; pt < p1; pt += BN) {
-          for (int kc = 0; kc < p.kchunks; ++kc) {
-            mbar_wait(&empty[stage], ph ^ 1);
+          // whole-tile stages: one stage = every K chunk of the B tile
+          const int per_stage = p.tile_stage ? p.kchunks : 1;
+          for (int kc0 = 0; kc0 < p.kchunks; kc0 += per_stage) {
+            mbar_wait_sleep(&empty[stage], ph ^ 1);
             unsigned char *dst = sb + stage * stage_bytes;
-            mbar_expect_tx(&full[stage], (uint32_t)stage_bytes);
-            tma_load_2d(dst, &map_p, &full[stage], kc * KCH, (int)pt);
-            if (kAStream)
-              tma_load_2d(dst + B_CHUNK, &map_c, &full[stage], kc * KCH, crow);
+            if (p.dbg & 4) {  // timing experiment: no operand traffic
+              mbar_arrive(&full[stage]);
+            } else {
+              mbar_expect_tx(&full[stage], (uint32_t)stage_bytes);
+              for (int j = 0; j < per_stage; ++j)
+                tma_load_2d(dst + j * B_CHUNK, &map_p, &full[stage],
+                            (kc0 + j) * KCH, (int)pt);
+              if (kAStream)
+                tma_load_2d(dst + B_CHUNK, &map_c, &full[stage], kc0 * KCH,
+                            crow);
+            }
             if (++stage == p.stages) {
               stage = 0;
               ph ^= 1;
@@ -240,103 +345,143 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    int stage = 0, buf = 0;
-    uint32_t ph = 0, aph = 0;
-    uint32_t tph[2] = {0, 0};
-    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
-      const int64_t sp = it / p.cand_tiles;
-      if (!kAStream) {
-        mbar_wait(afull, aph);
-        aph ^= 1;
-        fence_after();
-      }
-      const int64_t p0 = sp * p.split_pts;
-      const int64_t p1 = min(p.n, p0 + p.split_pts);
-      for (int64_t pt = p0; pt < p1; pt += BN) {
-        mbar_wait(&tempty[buf], tph[buf] ^ 1);
-        tph[buf] ^= 1;
-        fence_after();
-        const uint32_t dcol = tmem + (uint32_t)(buf * BN);
-        for (int kc = 0; kc < p.kchunks; ++kc) {
-          mbar_wait(&full[stage], ph);
-          fence_after();
-          unsigned char *bsm = sb + stage * stage_bytes;
-          const uint32_t abase =
-              kAStream ? su32(bsm + B_CHUNK) : su32(sa + kc * A_CHUNK);
-          const uint32_t bbase = su32(bsm);
-          const int k_lo = kc * (KCH / 16);
-          const int k_hi = min(p.ksteps, k_lo + KCH / 16);
-          if (lane == 0) {
-            for (int ks = k_lo; ks < k_hi; ++ks) {
-              const uint32_t off = (uint32_t)((ks - k_lo) * 32);
-              umma_f16(dcol, sw128_desc(abase + off), sw128_desc(bbase + off),
-                       p.idesc, (ks > 0) ? 1u : 0u);
+    // One thread runs the whole role.  With whole-tile stages the K-steps of
+    // a tile are issued back to back after a single barrier wait; the
+    // timeline tool (EXEM_TC_TRACE, tools/tc_trace.py) showed per-chunk
+    // synchronisation inside a tile costing ~2x in tensor-pipe time.
+    if (lane == 0) {
+      const uint64_t a_desc0 = sw128_desc(su32(sa));
+      const uint64_t b_desc0 = sw128_desc(su32(sb));
+      const uint32_t stage_step = (uint32_t)(stage_bytes >> 4);
+      int stage = 0;
+      uint32_t ph = 0, aph = 0, tph = 0;  // tph: bit b = phase of buffer b
+      uint32_t buf = 0;
+      int tile_no = 0;
+      for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+        const int64_t sp = it / p.cand_tiles;
+        if (!kAStream) {
+          mbar_wait(afull, aph);
+          aph ^= 1;
+        }
+        const int64_t p0 = sp * p.split_pts;
+        const int64_t p1 = min(p.n, p0 + p.split_pts);
+        for (int64_t pt = p0; pt < p1; pt += BN) {
+          TR(0, tile_no);
+          mbar_wait(&tempty[buf], ((tph >> buf) & 1u) ^ 1u);
+          TR(1, tile_no);
+          tph ^= 1u << buf;
+          fence_after();  // TMEM WAR vs the epilogue's tcgen05.ld
+          const uint32_t dcol = tmem + buf * (uint32_t)BN;
+          if (p.tile_stage) {
+            mbar_wait(&full[stage], ph);
+            TR(2, tile_no);
+            const uint64_t bd0 = b_desc0 + (uint64_t)(stage * stage_step);
+            if (!(p.dbg & 2)) {
+#pragma unroll 1
+              for (int ks = 0; ks < p.ksteps; ++ks) {
+                const uint32_t off_a = (uint32_t)((ks >> 2) * (A_CHUNK >> 4) + (ks & 3) * 2);
+                const uint32_t off_b = (uint32_t)((ks >> 2) * (B_CHUNK >> 4) + (ks & 3) * 2);
+                umma_f16(dcol, a_desc0 + off_a, bd0 + off_b, p.idesc,
+                         ks > 0 ? 1u : 0u);
+              }
             }
             umma_commit(&empty[stage]);
+            if (++stage == p.stages) {
+              stage = 0;
+              ph ^= 1;
+            }
+          } else {
+            int ks_left = p.ksteps;
+            for (int kc = 0; kc < p.kchunks; ++kc) {
+              mbar_wait(&full[stage], ph);
+              if (kc == 0) TR(2, tile_no);
+              const uint64_t bd = b_desc0 + (uint64_t)(stage * stage_step);
+              const uint64_t ad =
+                  kAStream ? bd + (uint64_t)(B_CHUNK >> 4)
+                           : a_desc0 + (uint64_t)(kc * (A_CHUNK >> 4));
+              const int nk = ks_left < KCH / 16 ? ks_left : KCH / 16;
+              if (!(p.dbg & 2)) {
+#pragma unroll 1
+                for (int j = 0; j < nk; ++j)
+                  umma_f16(dcol, ad + (uint64_t)(2 * j), bd + (uint64_t)(2 * j),
+                           p.idesc, (kc | j) ? 1u : 0u);
+              }
+              ks_left -= KCH / 16;
+              umma_commit(&empty[stage]);
+              if (++stage == p.stages) {
+                stage = 0;
+                ph ^= 1;
+              }
+            }
           }
-          __syncwarp();
-          if (++stage == p.stages) {
-            stage = 0;
-            ph ^= 1;
-          }
+          umma_commit(&tfull[buf]);
+          TR(3, tile_no);
+          ++tile_no;
+          buf ^= 1u;
         }
-        if (lane == 0) umma_commit(&tfull[buf]);
-        __syncwarp();
-        buf ^= 1;
-      }
-      if (!kAStream) {
-        if (lane == 0) umma_commit(aempty);
-        __syncwarp();
+        if (!kAStream) umma_commit(aempty);
       }
     }
+    __syncwarp();
   } else {
     // ------------------------------------------------------------ epilogue
     const int ew = warp - 2;            // 0..7
     const int q = warp & 3;             // TMEM lane quarter of this warp
     const int half = ew >> 2;           // column half of the 256-wide tile
     const int row = q * 32 + lane;      // candidate row within the tile
-    int buf = 0;
-    uint32_t tph[2] = {0, 0};
+    uint32_t buf = 0, tph = 0;  // tph: bit b = phase of buffer b
+    int tile_no = 0;
+    const bool tr = (warp == 2 && lane == 0);
     for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
       const int64_t ct = it % p.cand_tiles, sp = it / p.cand_tiles;
       const int64_t p0 = sp * p.split_pts;
       const int64_t p1 = min(p.n, p0 + p.split_pts);
       double g = 0.0;
       for (int64_t pt = p0; pt < p1; pt += BN) {
-        mbar_wait(&tfull[buf], tph[buf]);
-        tph[buf] ^= 1;
+        if (tr) TR(4, tile_no);
+        // one lane polls the barrier; the warp sync orders the others
+        if (lane == 0) mbar_wait_sleep(&tfull[buf], (tph >> buf) & 1u);
+        __syncwarp();
+        if (tr) TR(5, tile_no);
+        tph ^= 1u << buf;
         fence_after();
         const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) +
                                (uint32_t)(buf * BN + half * 128);
-        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-#pragma unroll
-        for (int h2 = 0; h2 < 2; ++h2) {
-          uint32_t r0[32], r1[32];
-          TMEM_LD32(taddr + h2 * 64, r0);
-          TMEM_LD32(taddr + h2 * 64 + 32, r1);
-          tmem_wait_ld();
-          if (h2 == 1) {
-            fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[buf]);
-          }
-#pragma unroll
-          for (int j = 0; j < 32; j += 4) {
-            s0 += fmaxf(__uint_as_float(r0[j]), 0.f);
-            s1 += fmaxf(__uint_as_float(r0[j + 1]), 0.f);
-            s2 += fmaxf(__uint_as_float(r0[j + 2]), 0.f);
-            s3 += fmaxf(__uint_as_float(r0[j + 3]), 0.f);
-          }
-#pragma unroll
-          for (int j = 0; j < 32; j += 4) {
-            s0 += fmaxf(__uint_as_float(r1[j]), 0.f);
-            s1 += fmaxf(__uint_as_float(r1[j + 1]), 0.f);
-            s2 += fmaxf(__uint_as_float(r1[j + 2]), 0.f);
-            s3 += fmaxf(__uint_as_float(r1[j + 3]), 0.f);
-          }
+        // Drain this warp's 32x128 slice of the accumulator into registers
+        // first and release the TMEM buffer immediately, so the MMA of tile
+        // t+2 never waits on this tile's arithmetic.
+        uint32_t r0[32], r1[32], r2[32], r3[32];
+        TMEM_LD32(taddr, r0);
+        TMEM_LD32(taddr + 32, r1);
+        TMEM_LD32(taddr + 64, r2);
+        TMEM_LD32(taddr + 96, r3);
+        tmem_wait_ld();
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[buf]);
+        if (tr) TR(6, tile_no);
+        if (p.dbg & 1) {  // timing experiment: no epilogue arithmetic
+          g += (double)__uint_as_float(r0[0] ^ r1[5] ^ r2[9] ^ r3[31]);
+          buf ^= 1u;
+          ++tile_no;
+          continue;
         }
+        // relu-sum with a sign-bit screen: max(0, D) contributes only where
+        // D >= +0, and almost every (candidate, point) pair has D < 0 (a
+        // candidate helps only points closer to it than their current
+        // exemplar).  AND-ing the raw bits of 32 values (LOP3, 3 inputs per
+        // op) leaves the sign bit set iff all 32 are negative, so the FMNMX +
+        // FADD work runs only for chunks that can contribute.  Skipped
+        // chunks would only have added +0, so the sums are bit-identical.
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+        if ((int)and32(r0) >= 0) relu_acc(r0, s0, s1);
+        if ((int)and32(r1) >= 0) relu_acc(r1, s2, s3);
+        if ((int)and32(r2) >= 0) relu_acc(r2, s0, s1);
+        if ((int)and32(r3) >= 0) relu_acc(r3, s2, s3);
         g += (double)((s0 + s1) + (s2 + s3));
-        buf ^= 1;
+        if (tr) TR(7, tile_no);
+        ++tile_no;
+        buf ^= 1u;
       }
       // fixed-order merge of the two column halves
       if (half == 1) red[row] = g;
@@ -520,13 +665,29 @@ int exem_greedy_gains_tc(int dtype, const void *xc, int64_t l, const void *xp,
   prm.kchunks = kchunks;
   prm.idesc = make_idesc(dtype == EXEM_BF16, BM, BN);
   prm.partial = partial;
+  {
+    const char *dbg = getenv("EXEM_TC_DEBUG");
+    prm.dbg = dbg ? atoi(dbg) : 0;
+  }
+  prm.trace = nullptr;
+  const char *trace_path = getenv("EXEM_TC_TRACE");
+  if (trace_path) {
+    cudaMalloc(&prm.trace, 16 * kTrace * sizeof(long long));
+    cudaMemset(prm.trace, 0, 16 * kTrace * sizeof(long long));
+  }
   // A stationary when it leaves room for >= 3 B chunk stages.
   const int avail = kSmemBudget - kBarBytes - 1024;
   const bool astream = (avail - kchunks * A_CHUNK) / B_CHUNK < 3;
-  const int stage_bytes = B_CHUNK + (astream ? A_CHUNK : 0);
+  // Whole-tile stages (one barrier handshake per B tile) when >= 3 fit.
+  const bool tile_stage =
+      !astream && (avail - kchunks * A_CHUNK) / (kchunks * B_CHUNK) >= 3;
+  const int stage_bytes = tile_stage ? kchunks * B_CHUNK
+                                     : B_CHUNK + (astream ? A_CHUNK : 0);
   int stages = (avail - (astream ? 0 : kchunks * A_CHUNK)) / stage_bytes;
   if (stages > 8) stages = 8;
+  if (const char *ms = getenv("EXEM_TC_STAGES")) stages = atoi(ms);  // timing only
   prm.stages = stages;
+  prm.tile_stage = tile_stage ? 1 : 0;
   const size_t smem = (size_t)(astream ? 0 : kchunks * A_CHUNK) +
                       (size_t)stages * stage_bytes + kBarBytes + 1024;
   CUtensorMap mc, mp;
@@ -552,6 +713,19 @@ int exem_greedy_gains_tc(int dtype, const void *xc, int64_t l, const void *xp,
     gains_tc_kernel<false><<<grid, kThreads, smem, st>>>(mc, mp, prm);
   }
   EXEM_LAUNCH_CHECK("gains_tc_kernel");
+  if (prm.trace) {  // timing experiment: dump the CTA-0 timeline
+    static long long host[16 * kTrace];
+    cudaStreamSynchronize(st);
+    cudaMemcpy(host, prm.trace, sizeof(host), cudaMemcpyDeviceToHost);
+    cudaFree(prm.trace);
+    if (FILE *f = fopen(trace_path, "w")) {
+      for (int t = 0; t < kTrace; ++t) {
+        for (int s = 0; s < 10; ++s)
+          fprintf(f, "%lld%c", host[s * kTrace + t], s == 9 ? '\n' : ' ');
+      }
+      fclose(f);
+    }
+  }
   return EXEM_OK;
 }
 
