@@ -177,6 +177,88 @@ __device__ __forceinline__ void umma_chunk_n(int nk, uint32_t d, uint64_t ad,
   }
 }
 
+// All K steps of one whole-tile stage, fully unrolled (compile-time
+// descriptor offsets): A chunks are A_CHUNK apart, B chunks B_CHUNK apart,
+// K=16 steps 32 B apart inside a 128-B swizzle row.
+template <int KS>
+__device__ __forceinline__ void issue_tile(uint32_t d, uint64_t a0,
+                                           uint64_t b0, uint32_t idesc) {
+#pragma unroll
+  for (int ks = 0; ks < KS; ++ks) {
+    constexpr uint32_t kA = 128 * 128 >> 4, kB = 256 * 128 >> 4;
+    umma_f16(d, a0 + (uint64_t)((ks >> 2) * kA + (ks & 3) * 2),
+             b0 + (uint64_t)((ks >> 2) * kB + (ks & 3) * 2), idesc,
+             ks > 0 ? 1u : 0u);
+  }
+}
+
+// MMAs [LO, HI) of one whole-tile stage.
+template <int LO, int HI>
+__device__ __forceinline__ void issue_range(uint32_t d, uint64_t a0,
+                                            uint64_t b0, uint32_t idesc) {
+#pragma unroll
+  for (int ks = LO; ks < HI; ++ks) {
+    constexpr uint32_t kA = 128 * 128 >> 4, kB = 256 * 128 >> 4;
+    umma_f16(d, a0 + (uint64_t)((ks >> 2) * kA + (ks & 3) * 2),
+             b0 + (uint64_t)((ks >> 2) * kB + (ks & 3) * 2), idesc,
+             ks > 0 ? 1u : 0u);
+  }
+}
+
+// MMA issuer state carried across work items.
+struct MmaState {
+  int stage;
+  uint32_t ph, tph, buf;
+  int tile_no;
+};
+
+// One work item (a split's point tiles against the stationary candidate
+// tile) with a software-pipelined handshake: the barrier waits for tile t+1
+// (accumulator buffer free, B stage landed) are placed between tile t's last
+// two MMAs, so their latency (~100-200 cycles each) hides behind queued
+// tensor work instead of opening a bubble in the ~2-deep MMA queue.
+template <int KS, typename P>
+__device__ __forceinline__ void mma_item_pipelined(
+    const P &p, int ntiles, MmaState &s, uint64_t a_desc0, uint64_t b_desc0,
+    uint32_t stage_step, uint32_t tmem, uint64_t *full, uint64_t *empty,
+    uint64_t *tfull, uint64_t *tempty) {
+  constexpr int H2 = KS > 2 ? KS - 2 : 0;
+  // acquire tile 0 of the item
+  mbar_wait(&tempty[s.buf], ((s.tph >> s.buf) & 1u) ^ 1u);
+  s.tph ^= 1u << s.buf;
+  mbar_wait(&full[s.stage], s.ph);
+  fence_after();
+  for (int t = 0; t < ntiles; ++t) {
+    const uint32_t d = tmem + s.buf * 256u;
+    const uint64_t b0 = b_desc0 + (uint64_t)(s.stage * stage_step);
+    const uint32_t nbuf = s.buf ^ 1u;
+    int nstage = s.stage + 1;
+    uint32_t nph = s.ph;
+    if (nstage == p.stages) {
+      nstage = 0;
+      nph ^= 1u;
+    }
+    issue_range<0, H2>(d, a_desc0, b0, p.idesc);
+    if (t + 1 < ntiles) {  // acquire tile t+1 while tile t's tail is queued
+      // (waiting earlier, e.g. after KS-4, was measured slower: tempty is
+      // usually not yet released there)
+      mbar_wait(&tempty[nbuf], ((s.tph >> nbuf) & 1u) ^ 1u);
+      s.tph ^= 1u << nbuf;
+      mbar_wait(&full[nstage], nph);
+      fence_after();
+    }
+    issue_range<H2, KS>(d, a_desc0, b0, p.idesc);
+    umma_commit(&empty[s.stage]);
+    umma_commit(&tfull[s.buf]);
+    if (p.trace != nullptr && blockIdx.x == 0 && s.tile_no < 256)
+      p.trace[3 * 256 + s.tile_no] = clock64();
+    ++s.tile_no;
+    s.buf = nbuf;
+    s.stage = nstage;
+    s.ph = nph;
+  }
+}
+
 // K-major, 128B-swizzled smem operand descriptor (tcgen05 "version 1").
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   uint64_t d = 0;
@@ -322,7 +404,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           // whole-tile stages: one stage = every K chunk of the B tile
           const int per_stage = p.tile_stage ? p.kchunks : 1;
           for (int kc0 = 0; kc0 < p.kchunks; kc0 += per_stage) {
-            mbar_wait_sleep(&empty[stage], ph ^ 1);
+            if (!(p.dbg & 16)) mbar_wait_sleep(&empty[stage], ph ^ 1);
             unsigned char *dst = sb + stage * stage_bytes;
             if (p.dbg & 4) {  // timing experiment: no operand traffic
               mbar_arrive(&full[stage]);
@@ -365,7 +447,30 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const int64_t p0 = sp * p.split_pts;
         const int64_t p1 = min(p.n, p0 + p.split_pts);
-        for (int64_t pt = p0; pt < p1; pt += BN) {
+        if (p.tile_stage && p.ksteps <= 8 && p.dbg == 0) {
+          // software-pipelined handshake (see mma_item_pipelined)
+          const int ntiles = (int)((p1 - p0 + BN - 1) / BN);
+          MmaState ms{stage, ph, tph, buf, tile_no};
+          const uint32_t st_step = stage_step;
+          switch (p.ksteps) {
+            case 1: mma_item_pipelined<1>(p, ntiles, ms, a_desc0, b_desc0, st_step, tmem, full, empty, tfull, tempty); break;
+            case 2: mma_item_pipelined<2>(p, ntiles, ms, a_desc0, b_desc0, st_step, tmem, full, empty, tfull, tempty); break;
+            case 3: mma_item_pipelined<3>(p, ntiles, ms, a_desc0, b_desc0, st_step, tmem, full, empty, tfull, tempty); break;
+            case 4: mma_item_pipelined<4>(p, ntiles, ms, a_desc0, b_desc0, st_step, tmem, full, empty, tfull, tempty); break;
+            case 5: mma_item_pipelined<5>(p, ntiles, ms, a_desc0, b_desc0, st_step, tmem, full, empty, tfull, tempty); break;
+            case 6: mma_item_pipelined<6>(p, ntiles, ms, a_desc0, b_desc0, st_step, tmem, full, empty, tfull, tempty); break;
+            case 7: mma_item_pipelined<7>(p, ntiles, ms, a_desc0, b_desc0, st_step, tmem, full, empty, tfull, tempty); break;
+            default: mma_item_pipelined<8>(p, ntiles, ms, a_desc0, b_desc0, st_step, tmem, full, empty, tfull, tempty); break;
+          }
+          stage = ms.stage;
+          ph = ms.ph;
+          tph = ms.tph;
+          buf = ms.buf;
+          tile_no = ms.tile_no;
+        }
+        for (int64_t pt = p0;
+             pt < p1 && !(p.tile_stage && p.ksteps <= 8 && p.dbg == 0);
+             pt += BN) {
           TR(0, tile_no);
           mbar_wait(&tempty[buf], ((tph >> buf) & 1u) ^ 1u);
           TR(1, tile_no);
@@ -373,19 +478,30 @@ __global__ void __launch_bounds__(kThreads, 1)
           fence_after();  // TMEM WAR vs the epilogue's tcgen05.ld
           const uint32_t dcol = tmem + buf * (uint32_t)BN;
           if (p.tile_stage) {
-            mbar_wait(&full[stage], ph);
+            if (!(p.dbg & 8)) mbar_wait(&full[stage], ph);
             TR(2, tile_no);
-            const uint64_t bd0 = b_desc0 + (uint64_t)(stage * stage_step);
+            const uint64_t bd0 = b_desc0 + (uint64_t)(((p.dbg & 128) ? 0 : stage) * stage_step);
             if (!(p.dbg & 2)) {
+              switch (p.ksteps) {  // compile-time K for d <= 122
+                case 1: issue_tile<1>(dcol, a_desc0, bd0, p.idesc); break;
+                case 2: issue_tile<2>(dcol, a_desc0, bd0, p.idesc); break;
+                case 3: issue_tile<3>(dcol, a_desc0, bd0, p.idesc); break;
+                case 4: issue_tile<4>(dcol, a_desc0, bd0, p.idesc); break;
+                case 5: issue_tile<5>(dcol, a_desc0, bd0, p.idesc); break;
+                case 6: issue_tile<6>(dcol, a_desc0, bd0, p.idesc); break;
+                case 7: issue_tile<7>(dcol, a_desc0, bd0, p.idesc); break;
+                case 8: issue_tile<8>(dcol, a_desc0, bd0, p.idesc); break;
+                default:
 #pragma unroll 1
-              for (int ks = 0; ks < p.ksteps; ++ks) {
-                const uint32_t off_a = (uint32_t)((ks >> 2) * (A_CHUNK >> 4) + (ks & 3) * 2);
-                const uint32_t off_b = (uint32_t)((ks >> 2) * (B_CHUNK >> 4) + (ks & 3) * 2);
-                umma_f16(dcol, a_desc0 + off_a, bd0 + off_b, p.idesc,
-                         ks > 0 ? 1u : 0u);
+                  for (int ks = 0; ks < p.ksteps; ++ks) {
+                    const uint32_t off_a = (uint32_t)((ks >> 2) * (A_CHUNK >> 4) + (ks & 3) * 2);
+                    const uint32_t off_b = (uint32_t)((ks >> 2) * (B_CHUNK >> 4) + (ks & 3) * 2);
+                    umma_f16(dcol, a_desc0 + off_a, bd0 + off_b, p.idesc,
+                             ks > 0 ? 1u : 0u);
+                  }
               }
             }
-            umma_commit(&empty[stage]);
+            if (!(p.dbg & 16)) umma_commit(&empty[stage]);
             if (++stage == p.stages) {
               stage = 0;
               ph ^= 1;
