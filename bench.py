@@ -297,8 +297,11 @@ def main():
                                peaks.get("bf16_tflops")))
         bound = "tensor"
     else:
-        peak = float(peaks.get("fp32_ffma_tflops", 74.4)) * (
-            0.5 if prec is pb.Precision.binary64 else 1.0)
+        simt = ROOT / "profiles" / "simt_peak.json"
+        sp_j = json.loads(simt.read_text()) if simt.exists() else {}
+        peak = float(sp_j.get("fp64_dfma_tflops", 37.2)
+                     if prec is pb.Precision.binary64
+                     else sp_j.get("fp32_ffma_tflops", 74.4))
         bound = "fp32-pipe" if prec is pb.Precision.binary32 else "fp64-pipe"
     traffic = None
     tfile = ROOT / "profiles" / "gains_tc_traffic.json"
@@ -344,7 +347,7 @@ def main():
                          else "gains_simt_kernel", "achieved": achieved,
                          "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                          "peak_source": f"{peak_src} "
-                         f"{'bf16_tflops_sustained' if half else 'FFMA spec'}",
+                         f"{'bf16_tflops_sustained' if half else 'profiles/simt_peak.json'}",
                          "traffic": traffic, "algorithmic_flop_per_launch": flop,
                          "kernel_ms_avg": gains_ms_local,
                          "kernel_share_of_step": gains_ms_local * args.steps / ms},

@@ -156,11 +156,36 @@ int exem_greedy_gains_tc(int dtype, const void *xc, int64_t l, const void *xp,
                          int64_t n, int64_t d, int64_t split_pts,
                          double *partial, int64_t splits, void *stream);
 
+/*
+ * K4-TC  batch_eval_tc -- explicit packed sets on tensor cores (bf16/f16).
+ * Replaces evaluate_batch / tiled_evaluate, pkg/src/exembatch/evaluate.py:
+ * 142-149,197-270, for half storage (same partial[splits][l] contract as
+ * exem_batch_eval).  Points on M (TMEM lanes), set elements on N:
+ *   xp   [tc_rows(n)][kp] point operand built by exem_tc_pack_points with
+ *        m = NULL (h_i = ||v_i||^2 / 2).
+ *   aux  [n] float aux distances (compute type).
+ *   xs   [tc_set_rows(l, k_max)][kp] set-tile operand (exem_tc_pack_sets).
+ * exem_tc_set_geometry: a set tile holds `spt` sets of `w` = round_up(k_max,
+ * 8) columns, MMA N = ncols; EXEM_ERR_UNSUPPORTED when k_max > 256 (the
+ * caller then uses exem_batch_eval).
+ */
+int exem_tc_set_geometry(int64_t k_max, int32_t *spt, int32_t *w,
+                         int32_t *ncols);
+int64_t exem_tc_set_rows(int64_t l, int64_t k_max);
+int exem_tc_pack_sets(int dtype, const void *packed, const double *pnorms,
+                      const int32_t *card, int64_t l, int64_t l_pad,
+                      int64_t k_max, int64_t d, void *xs, void *stream);
+int exem_batch_eval_tc(int dtype, const void *xp, int64_t n, const void *aux,
+                       const void *xs, int64_t l, int64_t k_max, int64_t d,
+                       int64_t split_pts, double *partial, int64_t splits,
+                       void *stream);
+
 /* Build the TC candidate operand from the SIMT layout (+ norms). */
 int exem_tc_pack_candidates(int dtype, const void *vt, int64_t ld, int64_t n,
                             int64_t d, const double *norms, void *xc,
                             void *stream);
-/* Build / refresh the TC point operand from the SIMT layout, norms and m. */
+/* Build / refresh the TC point operand from the SIMT layout, norms and m
+ * (m = NULL: h_i = ||v_i||^2/2, the K4-TC point operand). */
 int exem_tc_pack_points(int dtype, const void *vt, int64_t ld, int64_t n,
                         int64_t d, const double *norms, const void *m,
                         void *xp, void *stream);

@@ -68,6 +68,13 @@ _SIGNATURES = {
     "exem_row_norms": (c_int, [c_int, _P, c_int64, c_int64, c_int64, _P, _P]),
     "exem_packed_norms": (c_int, [c_int, _P, c_int64, c_int64, c_int64, _P,
                                   _P]),
+    "exem_tc_set_geometry": (c_int, [c_int64, _P, _P, _P]),
+    "exem_tc_set_rows": (c_int64, [c_int64, c_int64]),
+    "exem_tc_pack_sets": (c_int, [c_int, _P, _P, _P, c_int64, c_int64,
+                                  c_int64, c_int64, _P, _P]),
+    "exem_batch_eval_tc": (c_int, [c_int, _P, c_int64, _P, _P, c_int64,
+                                   c_int64, c_int64, c_int64, _P, c_int64,
+                                   _P]),
     "exem_launch_count": (c_int64, []),
 }
 

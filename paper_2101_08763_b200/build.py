@@ -16,8 +16,10 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libexem_b200.so"
-SOURCES = [CSRC / "exem_simt.cu", CSRC / "exem_tc.cu"]
-HEADERS = [CSRC / "exem_common.cuh", ROOT / "include" / "exem_b200.h"]
+SOURCES = [CSRC / "exem_simt.cu", CSRC / "exem_tc.cu",
+           CSRC / "exem_tc_batch.cu"]
+HEADERS = [CSRC / "exem_common.cuh", CSRC / "exem_tc_common.cuh",
+           ROOT / "include" / "exem_b200.h"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -1,0 +1,487 @@
+// exem_tc_batch.cu -- K4-TC: tcgen05 evaluation of a batch of EXPLICIT sets
+// (the paper's S_multi) at bf16/f16, sm_100a only.
+//
+// Replaces evaluate_batch / _reference_eval / tiled_evaluate over the packed
+// round-robin batch, pkg/src/exembatch/evaluate.py:142-149,197-270 and
+// core.py:331-346, for binary16/bfloat16 storage:
+//
+//   partial[split][j] = sum_{i in split} min(aux_i, min_{e<card_j} d(v_i, S_j[e]))
+//
+// One MMA row-dot gives D[i][e] = v_i.e - a_i/2 - b_e/2 = -d(v_i, e)/2 with
+//   point rows    y_i = [v_i, -h_hi,-h_mid,-h_lo, 1,1,1, 0..]   h = ||v_i||^2/2
+//   element rows  x_e = [e,   1,1,1, -b_hi,-b_mid,-b_lo, 0..]  b = ||e||^2/2
+// (the K3 operand formats with m = 0; constants split into three half
+// pieces, ~24-bit fidelity).  So min_e d = -2 max_e D: the epilogue is a
+// per-set max over that set's TMEM columns, then min with aux, then a sum.
+//
+// Operand roles: points on M (TMEM lanes, streamed by TMA per K chunk),
+// set elements on N (the "set tile", stationary in smem for a work item).
+// A set tile holds `spt` whole sets, each padded to `w` = round_up(k_max, 8)
+// columns; blank slots (e >= card_j) and padding columns are copies of the
+// set's element 0, so they never change a minimum and need no masking
+// (cf. the blank-slot rule, core.py:227-230).
+//
+// Roles (320 threads, 1 CTA/SM, persistent over (split, set tile) items):
+//   warp 0      TMA producer (set tile once per item; point K-chunks
+//               through a `stages`-deep ring)
+//   warp 1      TMEM allocator + single-thread MMA issuer (M=128 x
+//               N=ncols x K=16), handshakes software-pipelined one chunk
+//               ahead so the tensor pipe's ~2-deep queue never drains
+//   warps 2-9   epilogue: lane quarter q = warp%4 (TMEM lane access rule),
+//               set parity h = (warp-2)/4; per-thread fp64 running sums per
+//               set across the item's point tiles, fixed-order xor-shuffle +
+//               cross-quarter reduction at item end (deterministic).
+#include <cstdlib>
+
+#include "exem_tc_common.cuh"
+
+namespace exem {
+namespace tcb {
+
+using namespace exem::tc;
+
+constexpr int BM = 128;                 // points per tile (TMEM lanes)
+constexpr int A_CHUNK = BM * 128;       // bytes of one point K-chunk
+constexpr int kThreads = 320;
+constexpr int kEpiWarps = 8;
+constexpr int kMaxSpt = 32;             // sets per set tile (w >= 8)
+constexpr int kSetsPerWarp = kMaxSpt / 2;
+constexpr int kSmemBudget = 227 * 1024;
+constexpr int kBarBytes = 2048;
+
+struct BParams {
+  int64_t n;           // points of this slice
+  int64_t l;           // sets
+  int64_t split_pts;   // points per split (multiple of BM)
+  int64_t splits;
+  int64_t set_tiles;
+  int spt;             // sets per set tile
+  int w;               // TMEM columns per set (multiple of 8)
+  int ncols;           // MMA N (multiple of 16, >= spt * w)
+  int ksteps;          // K=16 MMA steps
+  int kchunks;         // 64-wide K chunks per operand row
+  int stages;          // point-chunk ring depth
+  int bstream;         // 1: set chunks streamed with the point chunks
+  uint32_t idesc;
+  const float *aux;    // [n] aux distances (compute type)
+  double *partial;     // [splits][l]
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    batch_tc_kernel(const __grid_constant__ CUtensorMap map_p,
+                    const __grid_constant__ CUtensorMap map_s,
+                    const BParams p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char *smem = (unsigned char *)(((uintptr_t)smem_raw + 1023) &
+                                          ~(uintptr_t)1023);
+  const int b_chunk = p.ncols * 128;  // bytes of one set-tile K-chunk
+  const int sb_bytes = p.bstream ? 0 : p.kchunks * b_chunk;
+  const int stage_bytes = A_CHUNK + (p.bstream ? b_chunk : 0);
+  unsigned char *sb = smem;                        // stationary set tile
+  unsigned char *sa = smem + sb_bytes;             // point-chunk ring
+  uint64_t *bars = (uint64_t *)(sa + p.stages * stage_bytes);
+  uint64_t *full = bars;                           // [stages]
+  uint64_t *empty = bars + p.stages;               // [stages]
+  uint64_t *tfull = bars + 2 * p.stages;           // [2]
+  uint64_t *tempty = tfull + 2;                    // [2]
+  uint64_t *bfull = tempty + 2;                    // [1]
+  uint64_t *bempty = bfull + 1;                    // [1]
+  uint32_t *tmem_slot = (uint32_t *)(bempty + 1);
+  double *red = (double *)(tmem_slot + 4);         // [4][kMaxSpt]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], kEpiWarps);
+    }
+    mbar_init(bfull, 1);
+    mbar_init(bempty, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&map_p));
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&map_s));
+  }
+  if (warp == 1) {
+    asm volatile(
+        "tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::
+            "r"(su32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int64_t items = p.set_tiles * p.splits;
+
+  if (warp == 0) {
+    // -------------------------------------------------------------- producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t ph = 0, bph = 0;
+      for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+        const int64_t st = it % p.set_tiles, sp = it / p.set_tiles;
+        const int srow = (int)(st * p.ncols);
+        if (!p.bstream) {
+          mbar_wait_sleep(bempty, bph ^ 1);
+          bph ^= 1;
+          mbar_expect_tx(bfull, (uint32_t)sb_bytes);
+          for (int kc = 0; kc < p.kchunks; ++kc)
+            tma_load_2d(sb + kc * b_chunk, &map_s, bfull, kc * KCH, srow);
+        }
+        const int64_t p0 = sp * p.split_pts;
+        const int64_t p1 = min(p.n, p0 + p.split_pts);
+        for (int64_t pt = p0; pt < p1; pt += BM) {
+          for (int kc = 0; kc < p.kchunks; ++kc) {
+            mbar_wait_sleep(&empty[stage], ph ^ 1);
+            unsigned char *dst = sa + stage * stage_bytes;
+            mbar_expect_tx(&full[stage], (uint32_t)stage_bytes);
+            tma_load_2d(dst, &map_p, &full[stage], kc * KCH, (int)pt);
+            if (p.bstream)
+              tma_load_2d(dst + A_CHUNK, &map_s, &full[stage], kc * KCH, srow);
+            if (++stage == p.stages) {
+              stage = 0;
+              ph ^= 1;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      const uint64_t a_base = sw128_desc(su32(sa));
+      const uint64_t b_base = sw128_desc(su32(sb));
+      const uint32_t a_step = (uint32_t)(stage_bytes >> 4);
+      const uint32_t b_step = (uint32_t)(b_chunk >> 4);
+      int stage = 0;
+      uint32_t ph = 0, bph = 0, tph = 0, buf = 0;
+      for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+        const int64_t sp = it / p.set_tiles;
+        const int64_t p0 = sp * p.split_pts;
+        const int64_t p1 = min(p.n, p0 + p.split_pts);
+        const int ntiles = (int)((p1 - p0 + BM - 1) / BM);
+        const int nev = ntiles * p.kchunks;
+        if (!p.bstream) {
+          mbar_wait(bfull, bph);
+          bph ^= 1;
+        }
+        // acquire event 0 (accumulator buffer free + point chunk landed)
+        mbar_wait(&tempty[buf], ((tph >> buf) & 1u) ^ 1u);
+        tph ^= 1u << buf;
+        mbar_wait(&full[stage], ph);
+        fence_after();
+        int kc = 0;
+        for (int e = 0; e < nev; ++e) {
+          const uint32_t d = tmem + buf * 256u;
+          const uint64_t ad = a_base + (uint64_t)(stage * a_step);
+          const uint64_t bd = p.bstream ? ad + (uint64_t)(A_CHUNK >> 4)
+                                        : b_base + (uint64_t)(kc * b_step);
+          const int rem = p.ksteps - kc * 4;
+          const int nk = rem < 4 ? rem : 4;
+          const int head = nk > 2 ? nk - 2 : 0;
+          const bool last = (kc == p.kchunks - 1);
+          int nstage = stage + 1;
+          uint32_t nph = ph;
+          if (nstage == p.stages) {
+            nstage = 0;
+            nph ^= 1u;
+          }
+#pragma unroll 1
+          for (int j = 0; j < head; ++j)
+            umma_f16(d, ad + (uint64_t)(2 * j), bd + (uint64_t)(2 * j),
+                     p.idesc, (kc | j) ? 1u : 0u);
+          if (e + 1 < nev) {  // acquire event e+1 behind the queued tail
+            if (last) {
+              const uint32_t nb = buf ^ 1u;
+              mbar_wait(&tempty[nb], ((tph >> nb) & 1u) ^ 1u);
+              tph ^= 1u << nb;
+            }
+            mbar_wait(&full[nstage], nph);
+            fence_after();
+          }
+#pragma unroll 1
+          for (int j = head; j < nk; ++j)
+            umma_f16(d, ad + (uint64_t)(2 * j), bd + (uint64_t)(2 * j),
+                     p.idesc, (kc | j) ? 1u : 0u);
+          umma_commit(&empty[stage]);
+          if (last) {
+            umma_commit(&tfull[buf]);
+            buf ^= 1u;
+            kc = 0;
+          } else {
+            ++kc;
+          }
+          stage = nstage;
+          ph = nph;
+        }
+        if (!p.bstream) umma_commit(bempty);
+      }
+    }
+    __syncwarp();
+  } else {
+    // -------------------------------------------------------------- epilogue
+    const int ew = warp - 2;       // 0..7
+    const int q = warp & 3;        // TMEM lane quarter
+    const int h = ew >> 2;         // set parity handled by this warp
+    const int row = q * 32 + lane; // point row within the tile
+    const int w8 = p.w >> 3;
+    uint32_t buf = 0, tph = 0;
+    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+      const int64_t st = it % p.set_tiles, sp = it / p.set_tiles;
+      const int64_t p0 = sp * p.split_pts;
+      const int64_t p1 = min(p.n, p0 + p.split_pts);
+      double acc[kSetsPerWarp];
+#pragma unroll
+      for (int u = 0; u < kSetsPerWarp; ++u) acc[u] = 0.0;
+      for (int64_t pt = p0; pt < p1; pt += BM) {
+        const int64_t pi = pt + row;
+        const bool valid = pi < p1;
+        const float ax = valid ? p.aux[pi] : 0.f;
+        if (lane == 0) mbar_wait_sleep(&tfull[buf], (tph >> buf) & 1u);
+        __syncwarp();
+        tph ^= 1u << buf;
+        fence_after();
+        const uint32_t taddr =
+            tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * 256);
+#pragma unroll
+        for (int u = 0; u < kSetsPerWarp; ++u) {
+          const int s = h + 2 * u;
+          if (s < p.spt) {  // warp-uniform
+            const uint32_t c0 = taddr + (uint32_t)(s * p.w);
+            float mx = -__int_as_float(0x7f800000);
+            for (int g = 0; g < w8; g += 4) {
+              uint32_t r[32];
+              TMEM_LD8(c0 + g * 8, r);
+              if (g + 1 < w8) TMEM_LD8(c0 + g * 8 + 8, r + 8);
+              if (g + 2 < w8) TMEM_LD8(c0 + g * 8 + 16, r + 16);
+              if (g + 3 < w8) TMEM_LD8(c0 + g * 8 + 24, r + 24);
+              tmem_wait_ld();
+#pragma unroll
+              for (int j = 0; j < 8; ++j) mx = fmaxf(mx, __uint_as_float(r[j]));
+              if (g + 1 < w8) {
+#pragma unroll
+                for (int j = 8; j < 16; ++j)
+                  mx = fmaxf(mx, __uint_as_float(r[j]));
+              }
+              if (g + 2 < w8) {
+#pragma unroll
+                for (int j = 16; j < 24; ++j)
+                  mx = fmaxf(mx, __uint_as_float(r[j]));
+              }
+              if (g + 3 < w8) {
+#pragma unroll
+                for (int j = 24; j < 32; ++j)
+                  mx = fmaxf(mx, __uint_as_float(r[j]));
+              }
+            }
+            // t_i = min(aux_i, max(0, min_e d)), min_e d = -2 max_e D
+            const float t = fminf(ax, fmaxf(0.f, -2.f * mx));
+            if (valid) acc[u] += (double)t;
+          }
+        }
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[buf]);
+        buf ^= 1u;
+      }
+      // item end: per set, fixed xor tree over the 32 lanes, then the four
+      // lane quarters in order
+#pragma unroll
+      for (int u = 0; u < kSetsPerWarp; ++u) {
+        const int s = h + 2 * u;
+        if (s < p.spt) {
+          double v = acc[u];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1)
+            v += __shfl_xor_sync(0xffffffffu, v, o);
+          if (lane == 0) red[q * kMaxSpt + s] = v;
+        }
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+      if (ew == 0 && lane < p.spt) {
+        const int64_t j = st * p.spt + lane;
+        if (j < p.l)
+          p.partial[sp * p.l + j] =
+              ((red[lane] + red[kMaxSpt + lane]) + red[2 * kMaxSpt + lane]) +
+              red[3 * kMaxSpt + lane];
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+    }
+  }
+
+  fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    fence_after();
+    asm volatile(
+        "tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// ---------------------------------------------------------------- packing
+// Set-tile operand rows from the packed round-robin batch
+// packed[d_pad][k_max][l_pad] (compute type, packed_address order,
+// core.py:320-328).  Row r = tile*ncols + s*w + e holds element
+// (e < card_j ? e : 0) of set j = tile*spt + s, then the folded constants;
+// rows of sets j >= l and padding columns past spt*w are zero.
+template <int DT>
+__global__ void pack_sets_kernel(const float *__restrict__ packed,
+                                 const double *__restrict__ pnorms,
+                                 const int32_t *__restrict__ card, int64_t l,
+                                 int64_t l_pad, int k_max, int d, int spt,
+                                 int w, int ncols, int64_t rows,
+                                 typename Traits<DT>::S *__restrict__ x,
+                                 int64_t kp) {
+  using S = typename Traits<DT>::S;
+  const int64_t r = (int64_t)blockIdx.x * blockDim.y + threadIdx.y;
+  if (r >= rows) return;
+  const int64_t tile = r / ncols;
+  const int c = (int)(r % ncols);
+  const int s = c / w, e = c % w;
+  const int64_t j = tile * spt + s;
+  const bool real = s < spt && j < l;
+  const int src = real ? (e < card[j] ? e : 0) : 0;
+  const int64_t ldp = (int64_t)k_max * l_pad;
+  for (int k = threadIdx.x; k < kp; k += blockDim.x) {
+    double v = 0.0;
+    if (real) {
+      if (k < d) {
+        v = (double)packed[(int64_t)k * ldp + (int64_t)src * l_pad + j];
+      } else if (k < d + 3) {
+        v = 1.0;
+      } else if (k < d + kTcConst) {
+        const double t = 0.5 * pnorms[(int64_t)src * l_pad + j];
+        const double t0 = (double)to_c(from_d<S>(t));
+        const double t1 = (double)to_c(from_d<S>(t - t0));
+        const double t2 = (double)to_c(from_d<S>(t - t0 - t1));
+        const int piece = k - d - 3;
+        v = -(piece == 0 ? t0 : (piece == 1 ? t1 : t2));
+      }
+    }
+    x[r * kp + k] = from_d<S>(v);
+  }
+}
+
+}  // namespace tcb
+}  // namespace exem
+
+using namespace exem;
+
+extern "C" {
+
+int exem_tc_set_geometry(int64_t k_max, int32_t *spt, int32_t *w,
+                         int32_t *ncols) {
+  if (k_max < 1) return fail(EXEM_ERR_ARG, "k_max must be >= 1");
+  const int64_t ww = round_up(k_max, 8);
+  if (ww > 256)
+    return fail(EXEM_ERR_UNSUPPORTED,
+                "tcgen05 batch path holds a set in <= 256 TMEM columns "
+                "(k_max=%lld)", (long long)k_max);
+  int64_t s = 256 / ww;
+  if (s > tcb::kMaxSpt) s = tcb::kMaxSpt;
+  *spt = (int32_t)s;
+  *w = (int32_t)ww;
+  *ncols = (int32_t)round_up(s * ww, 16);
+  return EXEM_OK;
+}
+
+int64_t exem_tc_set_rows(int64_t l, int64_t k_max) {
+  int32_t spt, w, nc;
+  if (exem_tc_set_geometry(k_max, &spt, &w, &nc) != EXEM_OK) return -1;
+  return ceil_div(l < 1 ? 1 : l, spt) * nc;
+}
+
+int exem_tc_pack_sets(int dtype, const void *packed, const double *pnorms,
+                      const int32_t *card, int64_t l, int64_t l_pad,
+                      int64_t k_max, int64_t d, void *xs, void *stream) {
+  if (dtype != EXEM_BF16 && dtype != EXEM_F16)
+    return fail(EXEM_ERR_ARG, "TC operands are bf16/f16 only");
+  int32_t spt, w, nc;
+  if (int rc = exem_tc_set_geometry(k_max, &spt, &w, &nc)) return rc;
+  const int64_t rows = exem_tc_set_rows(l, k_max);
+  const int64_t kp = exem_tc_kp(d);
+  dim3 block(64, 4);
+  dim3 grid((unsigned)ceil_div(rows, 4));
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == EXEM_BF16)
+    tcb::pack_sets_kernel<EXEM_BF16><<<grid, block, 0, st>>>(
+        (const float *)packed, pnorms, card, l, l_pad, (int)k_max, (int)d, spt,
+        w, nc, rows, (__nv_bfloat16 *)xs, kp);
+  else
+    tcb::pack_sets_kernel<EXEM_F16><<<grid, block, 0, st>>>(
+        (const float *)packed, pnorms, card, l, l_pad, (int)k_max, (int)d, spt,
+        w, nc, rows, (__half *)xs, kp);
+  EXEM_LAUNCH_CHECK("tc_pack_sets");
+  return EXEM_OK;
+}
+
+int exem_batch_eval_tc(int dtype, const void *xp, int64_t n, const void *aux,
+                       const void *xs, int64_t l, int64_t k_max, int64_t d,
+                       int64_t split_pts, double *partial, int64_t splits,
+                       void *stream) {
+  using namespace exem::tcb;
+  if (dtype != EXEM_BF16 && dtype != EXEM_F16)
+    return fail(EXEM_ERR_ARG, "batch_eval_tc is bf16/f16 only");
+  if (n < 1 || l < 1) return fail(EXEM_ERR_ARG, "empty batch or ground set");
+  if (split_pts < BM || split_pts % BM)
+    return fail(EXEM_ERR_ARG, "split_pts must be a multiple of %d", BM);
+  if (splits != ceil_div(n, split_pts))
+    return fail(EXEM_ERR_ARG, "splits mismatch");
+  int dev = 0, sms = 0, major = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  if (major != 10)
+    return fail(EXEM_ERR_UNSUPPORTED,
+                "tcgen05 path needs an sm_100 (B200) device, found sm_%d",
+                major * 10);
+  BParams prm;
+  int32_t spt, w, nc;
+  if (int rc = exem_tc_set_geometry(k_max, &spt, &w, &nc)) return rc;
+  const int64_t kp = exem_tc_kp(d);
+  prm.n = n;
+  prm.l = l;
+  prm.split_pts = split_pts;
+  prm.splits = splits;
+  prm.set_tiles = ceil_div(l, spt);
+  prm.spt = spt;
+  prm.w = w;
+  prm.ncols = nc;
+  prm.ksteps = (int)ceil_div(d + kTcConst, 16);
+  prm.kchunks = (int)(kp / KCH);
+  prm.idesc = make_idesc(dtype == EXEM_BF16, BM, nc);
+  prm.aux = (const float *)aux;
+  prm.partial = partial;
+  const int b_chunk = nc * 128;
+  const int avail = kSmemBudget - kBarBytes - 1024;
+  // set tile stationary when it leaves room for >= 3 point-chunk stages
+  const bool bstream = (avail - prm.kchunks * b_chunk) / A_CHUNK < 3;
+  const int sb_bytes = bstream ? 0 : prm.kchunks * b_chunk;
+  const int stage_bytes = A_CHUNK + (bstream ? b_chunk : 0);
+  int stages = (avail - sb_bytes) / stage_bytes;
+  if (stages > 8) stages = 8;
+  if (stages < 2) return fail(EXEM_ERR_UNSUPPORTED, "set tile too large for smem");
+  prm.stages = stages;
+  prm.bstream = bstream ? 1 : 0;
+  const size_t smem = (size_t)sb_bytes + (size_t)stages * stage_bytes +
+                      kBarBytes + 1024;
+  CUtensorMap mp, ms;
+  if (int rc = make_map(&mp, xp, dtype, exem_tc_rows(n), kp, BM)) return rc;
+  if (int rc = make_map(&ms, xs, dtype, exem_tc_set_rows(l, k_max), kp, nc))
+    return rc;
+  const int64_t items = prm.set_tiles * splits;
+  const unsigned grid = (unsigned)(items < sms ? items : sms);
+  cudaError_t e = cudaFuncSetAttribute(
+      batch_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess)
+    return fail(EXEM_ERR_CUDA, "smem attr: %s", cudaGetErrorString(e));
+  batch_tc_kernel<<<grid, kThreads, smem, (cudaStream_t)stream>>>(mp, ms, prm);
+  EXEM_LAUNCH_CHECK("batch_tc_kernel");
+  return EXEM_OK;
+}
+
+}  // extern "C"

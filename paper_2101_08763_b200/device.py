@@ -8,6 +8,8 @@ stream provider) the device layouts described in DESIGN.md:
 * ``norms``  [ld]  f64     ||v_i||^2 of the stored values.
 * ``aux``    [ld]  compute d(v_i, e0) rounded through the storage dtype.
 * ``xc``     [rows][kp]    bf16/f16 tensor-core candidate operand (lazy).
+* ``xp0``    [rows][kp]    bf16/f16 tensor-core point operand, m = 0 (lazy;
+                           the point side of the K4-TC batch kernel).
 
 Everything numeric is done by the kernels of ``libexem_b200.so``.
 """
@@ -105,11 +107,26 @@ class DeviceGround:
                                dtype=t.float64, device=self.dev)
         self.aux_sum = t.empty(1, dtype=t.float64, device=self.dev)
         self._xc = None
+        self._xp0 = None
         self.kp = int(lib.tc_kp(self.d)) if precision.is_half else 0
 
     @property
     def stream(self):
         return N.stream_handle(self.dev)
+
+    def xp0(self):
+        """Tensor-core point operand with h_i = ||v_i||^2/2 (m = 0): the
+        point side of K4-TC (built once)."""
+        if self._xp0 is None:
+            t = torch()
+            lib = N.lib()
+            rows = int(lib.tc_rows(self.n))
+            tdt = t.bfloat16 if self.precision.tag == N.BF16 else t.float16
+            self._xp0 = t.empty((rows, self.kp), dtype=tdt, device=self.dev)
+            lib.tc_pack_points(self.precision.tag, N.ptr(self.vt), self.ld,
+                               self.n, self.d, N.ptr(self.norms), None,
+                               N.ptr(self._xp0), self.stream)
+        return self._xp0
 
     def xc(self):
         """Tensor-core candidate operand [tc_rows][kp] (built once)."""

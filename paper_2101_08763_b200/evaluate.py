@@ -129,9 +129,72 @@ def evaluate_single(ground: GroundSet, set_vectors,
     return float(_finish(ground, np.array([total]))[0])
 
 
+TC_MAX_SET = 256  # K4-TC holds one set in <= 256 TMEM columns
+
+
+def tc_batch_supported(precision: Precision, k_max: int) -> bool:
+    """Explicit batches of half-precision ground sets run on tensor cores
+    (K4-TC) when a set fits one TMEM tile; otherwise on the SIMT K4."""
+    return precision.is_half and 1 <= k_max <= TC_MAX_SET
+
+
+class DeviceBatch:
+    """A packed batch uploaded once (packed_address order, core.py:320-328)
+    plus what the batch kernels need: element norms, cardinalities and, for
+    half precision, the K4-TC set-tile operand."""
+
+    def __init__(self, values: np.ndarray, d: int, k_max: int, l: int,
+                 cardinalities, precision: Precision, d_pad: int, dev,
+                 stream):
+        from .device import torch
+
+        t = torch()
+        lib = N.lib()
+        self.d, self.k_max, self.l = d, k_max, l
+        self.l_pad = int(-(-l // 128) * 128)
+        self.precision = precision
+        host = np.zeros((d_pad, k_max, self.l_pad),
+                        dtype=precision.compute_dtype)
+        host[:d, :, :l] = np.asarray(values, dtype=precision.dtype).reshape(
+            d, k_max, l).astype(precision.compute_dtype)
+        self.packed = t.from_numpy(host).to(dev)
+        self.pnorms = t.empty((k_max, self.l_pad), dtype=t.float64, device=dev)
+        lib.packed_norms(precision.tag, N.ptr(self.packed), d, k_max,
+                         self.l_pad, N.ptr(self.pnorms), stream)
+        self.card = t.tensor(np.asarray(cardinalities, dtype=np.int32),
+                             device=dev)
+        self.xs = None
+        if tc_batch_supported(precision, k_max):
+            rows = int(lib.tc_set_rows(l, k_max))
+            tdt = t.bfloat16 if precision.tag == N.BF16 else t.float16
+            self.xs = t.empty((rows, int(lib.tc_kp(d))), dtype=tdt,
+                              device=dev)
+            lib.tc_pack_sets(precision.tag, N.ptr(self.packed),
+                             N.ptr(self.pnorms), N.ptr(self.card), l,
+                             self.l_pad, k_max, d, N.ptr(self.xs), stream)
+
+
+def batch_partials(dg, batch: DeviceBatch, partial, split_pts: int,
+                   splits: int) -> None:
+    """K4 (SIMT) or K4-TC over the ground rows held by ``dg``:
+    partial[s][j] = sum over split s of t_i(S_j)."""
+    lib = N.lib()
+    prec = dg.precision
+    if batch.xs is not None:
+        lib.batch_eval_tc(prec.tag, N.ptr(dg.xp0()), dg.n, N.ptr(dg.aux),
+                          N.ptr(batch.xs), batch.l, batch.k_max, dg.d,
+                          split_pts, N.ptr(partial), splits, dg.stream)
+    else:
+        lib.batch_eval(prec.tag, N.ptr(dg.vt), dg.ld, dg.n, dg.d,
+                       N.ptr(dg.norms), N.ptr(dg.aux), N.ptr(batch.packed),
+                       N.ptr(batch.pnorms), N.ptr(batch.card), batch.l,
+                       batch.l_pad, batch.k_max, split_pts, N.ptr(partial),
+                       splits, dg.stream)
+
+
 def device_packed_sums(ground: GroundSet, values: np.ndarray, d: int,
                        k_max: int, l: int, cardinalities, device=None):
-    """Upload a packed (d, k_max, l) buffer and run K4 + K6.
+    """Upload a packed (d, k_max, l) buffer and run K4 (or K4-TC) + K6.
 
     Returns the device tensor of per-set fp64 sums sum_i t_i(S_j).
     """
@@ -140,24 +203,12 @@ def device_packed_sums(ground: GroundSet, values: np.ndarray, d: int,
     t = torch()
     lib = N.lib()
     dg = ground.on_device(device)
-    prec = ground.precision
-    l_pad = int(-(-l // 128) * 128)
     with t.cuda.device(dg.device_index):
         st = dg.stream
-        host = np.zeros((dg.d_pad, k_max, l_pad), dtype=prec.compute_dtype)
-        host[:d, :, :l] = np.asarray(values, dtype=prec.dtype).reshape(
-            d, k_max, l).astype(prec.compute_dtype)
-        packed = t.from_numpy(host).to(dg.dev)
-        pnorms = t.empty((k_max, l_pad), dtype=t.float64, device=dg.dev)
-        lib.packed_norms(prec.tag, N.ptr(packed), dg.d, k_max, l_pad,
-                         N.ptr(pnorms), st)
-        card = t.tensor(np.asarray(cardinalities, dtype=np.int32),
-                        device=dg.dev)
+        batch = DeviceBatch(values, d, k_max, l, cardinalities,
+                            ground.precision, dg.d_pad, dg.dev, st)
         partial = t.empty((dg.splits, l), dtype=t.float64, device=dg.dev)
-        lib.batch_eval(prec.tag, N.ptr(dg.vt), dg.ld, dg.n, dg.d,
-                       N.ptr(dg.norms), N.ptr(dg.aux), N.ptr(packed),
-                       N.ptr(pnorms), N.ptr(card), l, l_pad, k_max,
-                       dg.split_pts, N.ptr(partial), dg.splits, st)
+        batch_partials(dg, batch, partial, dg.split_pts, dg.splits)
         sums = t.empty(l, dtype=t.float64, device=dg.dev)
         lib.reduce_partials(N.ptr(partial), dg.splits, l, 1.0, N.ptr(sums), st)
     return sums

@@ -1,0 +1,83 @@
+// simt_peak.cu -- FP32 FFMA / FP64 DFMA throughput microbenchmark (B200).
+//
+// The roofline denominators for the SIMT kernels (K3-SIMT, K4 at f32/f64)
+// are not in MEASURED_PEAKS.json (which holds HBM copy and cuBLAS bf16), so
+// this measures them: every thread runs 8 independent FMA chains for a fixed
+// trip count, grid = SMs x 4 CTAs x 256 threads, CUDA events around the
+// launch, best of 10.  Also reports cycles via clock64 on CTA 0 so the rate
+// can be normalised per SM clock.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o simt_peak simt_peak.cu
+//   ./simt_peak   -> one JSON line
+#include <cuda_runtime.h>
+#include <stdio.h>
+
+template <typename T>
+__global__ void __launch_bounds__(256) fma_loop(T *out, int iters, T a, T b,
+                                                long long *cyc) {
+  T x0 = (T)threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4,
+    x5 = x0 + 5, x6 = x0 + 6, x7 = x0 + 7;
+  const long long c0 = clock64();
+#pragma unroll 1
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b);
+      x3 = fma(x3, a, b); x4 = fma(x4, a, b); x5 = fma(x5, a, b);
+      x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+    }
+  }
+  const long long c1 = clock64();
+  if (blockIdx.x == 0 && threadIdx.x == 0) *cyc = c1 - c0;
+  out[blockIdx.x * blockDim.x + threadIdx.x] =
+      x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+}
+
+template <typename T>
+static double run(int sms, int iters, double *ghz) {
+  const int blocks = sms * 4, threads = 256;
+  T *out;
+  long long *cyc;
+  cudaMalloc(&out, sizeof(T) * blocks * threads);
+  cudaMalloc(&cyc, sizeof(long long));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  fma_loop<T><<<blocks, threads>>>(out, iters / 10, (T)0.999, (T)0.001, cyc);
+  cudaDeviceSynchronize();
+  float best = 1e30f;
+  long long cbest = 0;
+  for (int r = 0; r < 10; ++r) {
+    cudaEventRecord(e0);
+    fma_loop<T><<<blocks, threads>>>(out, iters, (T)0.999, (T)0.001, cyc);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (ms < best) {
+      best = ms;
+      cudaMemcpy(&cbest, cyc, sizeof(cbest), cudaMemcpyDeviceToHost);
+    }
+  }
+  const double fmas = (double)blocks * threads * iters * 16 * 8;
+  *ghz = (double)cbest / (best * 1e-3) / 1e9;  // CTA-0 cycles / wall time
+  cudaFree(out);
+  cudaFree(cyc);
+  return 2.0 * fmas / (best * 1e-3) / 1e12;  // TFLOP/s
+}
+
+int main() {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  double g32, g64;
+  const double f32 = run<float>(sms, 20000, &g32);
+  const double f64 = run<double>(sms, 4000, &g64);
+  (void)g32;
+  (void)g64;
+  printf("{\"sm_count\": %d, \"fp32_ffma_tflops\": %.2f,"
+         " \"fp64_dfma_tflops\": %.2f,"
+         " \"how\": \"8 independent FMA chains/thread, %d SMs x 4 CTAs x 256 thr,"
+         " best of 10, CUDA events\"}\n",
+         sms, f32, f64, sms);
+  return 0;
+}
