@@ -86,6 +86,27 @@ int exem_ground_prepare(int dtype, const void *src, int64_t n, int64_t d,
                         void *stream);
 
 /*
+ * Low-memory regime (north-star item c): V stays in (pinned) host memory and
+ * streams through the device in split-aligned row slices.
+ *   exem_host_register / _unregister  page-lock an existing host buffer
+ *            (the F-order GroundSet.data, core.py:152-155) for async DMA.
+ *   exem_h2d_rows  rows [row0, row0+rows) of a column-major [d][ld_host]
+ *            host matrix -> a dense [d][rows] device buffer (one 2-D DMA).
+ *   exem_sum_fixed out[out_index] = fixed-order sum of `count` block
+ *            partials (the final step of K1/K2 sums; with per-slice block
+ *            partials at their global offsets the result is bit-identical
+ *            to the resident computation).
+ * K1 with aux_sum == NULL and K2 with sum_out == NULL leave their
+ * per-256-point block partials in `scratch` instead of reducing them.
+ */
+int exem_host_register(void *host, int64_t bytes);
+int exem_host_unregister(void *host);
+int exem_h2d_rows(void *dst, const void *host, int64_t ld_host, int64_t row0,
+                  int64_t rows, int64_t d, int64_t elem_bytes, void *stream);
+int exem_sum_fixed(const double *in, int64_t count, double *out,
+                   int64_t out_index, void *stream);
+
+/*
  * K2  set_min -- per-point minimum over one explicit element set
  * Replaces min_distances, pkg/src/exembatch/objective.py:113-141, and the
  * sum inside _set_value, pkg/src/exembatch/evaluate.py:105-112.

@@ -75,6 +75,11 @@ _SIGNATURES = {
     "exem_batch_eval_tc": (c_int, [c_int, _P, c_int64, _P, _P, c_int64,
                                    c_int64, c_int64, c_int64, _P, c_int64,
                                    _P]),
+    "exem_host_register": (c_int, [_P, c_int64]),
+    "exem_host_unregister": (c_int, [_P]),
+    "exem_h2d_rows": (c_int, [_P, _P, c_int64, c_int64, c_int64, c_int64,
+                              c_int64, _P]),
+    "exem_sum_fixed": (c_int, [_P, c_int64, _P, c_int64, _P]),
     "exem_launch_count": (c_int64, []),
 }
 

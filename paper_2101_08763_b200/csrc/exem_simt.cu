@@ -702,7 +702,52 @@ int exem_ground_prepare(int dtype, const void *src, int64_t n, int64_t d,
         (C *)aux, scratch);
     EXEM_LAUNCH_CHECK("ground_prepare_kernel");
   });
+  // aux_sum == NULL: leave the per-256-point block partials in scratch (a
+  // streamed slice writes them at its global block offset; exem_sum_fixed
+  // then reduces all of them in the same order as a resident build).
+  if (!aux_sum) return EXEM_OK;
   return reduce_fixed(scratch, blocks, aux_sum, 0, st);
+}
+
+int exem_sum_fixed(const double *in, int64_t count, double *out,
+                   int64_t out_index, void *stream) {
+  if (count < 1) return fail(EXEM_ERR_ARG, "sum_fixed: count must be >= 1");
+  return reduce_fixed(in, count, out, out_index, (cudaStream_t)stream);
+}
+
+int exem_host_register(void *host, int64_t bytes) {
+  cudaError_t e = cudaHostRegister(host, (size_t)bytes, cudaHostRegisterDefault);
+  if (e == cudaErrorHostMemoryAlreadyRegistered) {
+    cudaGetLastError();
+    return EXEM_OK;
+  }
+  if (e != cudaSuccess)
+    return fail(EXEM_ERR_CUDA, "cudaHostRegister: %s", cudaGetErrorString(e));
+  return EXEM_OK;
+}
+
+int exem_host_unregister(void *host) {
+  cudaError_t e = cudaHostUnregister(host);
+  if (e != cudaSuccess && e != cudaErrorHostMemoryNotRegistered)
+    return fail(EXEM_ERR_CUDA, "cudaHostUnregister: %s", cudaGetErrorString(e));
+  cudaGetLastError();
+  return EXEM_OK;
+}
+
+int exem_h2d_rows(void *dst, const void *host, int64_t ld_host, int64_t row0,
+                  int64_t rows, int64_t d, int64_t elem_bytes, void *stream) {
+  if (rows < 1 || d < 1 || row0 < 0 || row0 + rows > ld_host)
+    return fail(EXEM_ERR_ARG, "h2d_rows: bad slice [%lld, %lld) of %lld",
+                (long long)row0, (long long)(row0 + rows), (long long)ld_host);
+  const char *src = (const char *)host + row0 * elem_bytes;
+  cudaError_t e = cudaMemcpy2DAsync(dst, (size_t)(rows * elem_bytes), src,
+                                    (size_t)(ld_host * elem_bytes),
+                                    (size_t)(rows * elem_bytes), (size_t)d,
+                                    cudaMemcpyHostToDevice,
+                                    (cudaStream_t)stream);
+  if (e != cudaSuccess)
+    return fail(EXEM_ERR_CUDA, "h2d_rows: %s", cudaGetErrorString(e));
+  return EXEM_OK;
 }
 
 int exem_set_min(int dtype, const void *vt, int64_t ld, int64_t n, int64_t d,

@@ -16,6 +16,13 @@ matrix W split by columns across GPUs.
 
 The collective logic is written against a small ``ShardOps`` interface so
 the multi-process CPU tests (gloo, world_size 2) can drive the same loop.
+
+Explicit batches (``sharded_batch_sums``, BASELINE config 5) shard the same
+way: each rank streams its split-aligned rows through K4 / K4-TC into its
+rows of the [splits][l] partial matrix, the other rows stay zero, and one
+all-reduce(sum) of that matrix reconstructs every partial exactly (x + 0 is
+exact), so the fixed-order K6 reduce gives per-set sums bit-identical to a
+single GPU for any number of ranks.
 """
 
 from __future__ import annotations
@@ -143,3 +150,53 @@ def sharded_greedy(sg: ShardedGround, k: int, group=None):
     ms = msum.cpu().numpy()[:k]
     vals = acc.type(sg.aux_loss) - ms.astype(acc) / acc.type(sg.n)
     return tuple(int(i) for i in picks), tuple(float(v) for v in vals)
+
+
+def combine_partials(partial, all_reduce) -> None:
+    """All-reduce a [splits][l] partial matrix whose rows are owned by
+    exactly one rank (zeros elsewhere): exact, order-independent."""
+    all_reduce(partial)
+
+
+def sharded_batch_sums(ground, batch, rank: int, world: int, group=None,
+                       device=None, budget=None):
+    """Per-set fp64 sums of an explicit batch over a row-sharded V.
+
+    Rank ``rank`` evaluates every set against its rows [r0, r1) (whole
+    splits, ``shard_rows``), streamed through ``budget`` bytes of device
+    memory (default: the ground set's budget, else 80 % of free memory).
+    Returns the device tensor of l sums, identical on every rank.
+    """
+    import torch
+    import torch.distributed as dist
+
+    from . import _native as N
+    from .core import pack_batch
+    from .streaming import stream_packed_sums
+
+    lib = N.lib()
+    n = ground.n
+    sp = int(lib.split_points(n))
+    splits = -(-n // sp)
+    r0, r1 = shard_rows(n, world, rank, sp)
+    packed = pack_batch(batch, ground.precision)
+    dev = torch.device("cuda", torch.cuda.current_device()
+                       if device is None else device)
+    partial = torch.zeros((splits, packed.l), dtype=torch.float64, device=dev)
+    if budget is None:
+        budget = ground.device_budget or int(
+            0.8 * torch.cuda.mem_get_info(dev)[0])
+    if r1 > r0:
+        stream_packed_sums(ground, packed.values, packed.d, packed.k_max,
+                           packed.l, packed.cardinalities, dev.index,
+                           rows=(r0, r1), partial=partial, budget=budget)
+
+    def all_reduce(t):
+        if world > 1 and dist.is_available() and dist.is_initialized():
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+
+    combine_partials(partial, all_reduce)
+    sums = torch.empty(packed.l, dtype=torch.float64, device=dev)
+    lib.reduce_partials(N.ptr(partial), splits, packed.l, 1.0, N.ptr(sums),
+                        N.stream_handle(dev))
+    return sums

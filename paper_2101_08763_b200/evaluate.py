@@ -180,16 +180,17 @@ def batch_partials(dg, batch: DeviceBatch, partial, split_pts: int,
     partial[s][j] = sum over split s of t_i(S_j)."""
     lib = N.lib()
     prec = dg.precision
+    pp = partial if isinstance(partial, N.c_void_p) else N.ptr(partial)
     if batch.xs is not None:
         lib.batch_eval_tc(prec.tag, N.ptr(dg.xp0()), dg.n, N.ptr(dg.aux),
                           N.ptr(batch.xs), batch.l, batch.k_max, dg.d,
-                          split_pts, N.ptr(partial), splits, dg.stream)
+                          split_pts, pp, splits, dg.stream)
     else:
         lib.batch_eval(prec.tag, N.ptr(dg.vt), dg.ld, dg.n, dg.d,
                        N.ptr(dg.norms), N.ptr(dg.aux), N.ptr(batch.packed),
                        N.ptr(batch.pnorms), N.ptr(batch.card), batch.l,
-                       batch.l_pad, batch.k_max, split_pts, N.ptr(partial),
-                       splits, dg.stream)
+                       batch.l_pad, batch.k_max, split_pts, pp, splits,
+                       dg.stream)
 
 
 def device_packed_sums(ground: GroundSet, values: np.ndarray, d: int,
@@ -200,6 +201,11 @@ def device_packed_sums(ground: GroundSet, values: np.ndarray, d: int,
     """
     from .device import torch
 
+    if ground.streamed:
+        from .streaming import stream_packed_sums
+
+        return stream_packed_sums(ground, values, d, k_max, l, cardinalities,
+                                  device)
     t = torch()
     lib = N.lib()
     dg = ground.on_device(device)

@@ -167,6 +167,11 @@ def device_set_min(ground: GroundSet, elems: np.ndarray, include_aux: bool,
     """
     from .device import padded_rows, torch
 
+    if ground.streamed:
+        from .streaming import stream_set_min
+
+        return stream_set_min(ground, elems, include_aux, want_t, want_labels,
+                              device)
     t = torch()
     lib = N.lib()
     dg = ground.on_device(device)
