@@ -259,6 +259,14 @@ int exem_distance_matrix(int dtype, const void *a, const double *anorms,
                          int64_t q, int64_t d, int64_t d_pad, void *out,
                          void *stream);
 
+/* Packed round-robin batch [d_pad][k_max][l_pad] (compute type) from the
+ * concatenated element rows of the l sets: rows[offsets[j] + e][d] (storage
+ * dtype, row-major), card[j] = |S_j|; blank slots / padding are zero.  The
+ * device-side form of pack_batch, pkg/src/exembatch/core.py:331-346. */
+int exem_pack_elements(int dtype, const void *rows, const int64_t *offsets,
+                       const int32_t *card, int64_t l, int64_t l_pad,
+                       int64_t k_max, int64_t d, void *packed, void *stream);
+
 /* pnorms[e][j] = ||S_j[e]||^2 of a packed [d_pad][k_max][l_pad] batch
  * (the element norms e2 of objective.py:84, computed once per batch). */
 int exem_packed_norms(int dtype, const void *packed, int64_t d, int64_t k_max,

@@ -80,6 +80,8 @@ _SIGNATURES = {
     "exem_h2d_rows": (c_int, [_P, _P, c_int64, c_int64, c_int64, c_int64,
                               c_int64, _P]),
     "exem_sum_fixed": (c_int, [_P, c_int64, _P, c_int64, _P]),
+    "exem_pack_elements": (c_int, [c_int, _P, _P, _P, c_int64, c_int64,
+                                   c_int64, c_int64, _P, _P]),
     "exem_launch_count": (c_int64, []),
 }
 

@@ -635,6 +635,30 @@ __global__ void packed_norms_kernel(const C *__restrict__ packed, int d,
   out[idx] = s;
 }
 
+// Packed round-robin batch from element rows: packed[k][e][j] = the k-th
+// coordinate of element e of set j (packed_address order, core.py:320-328),
+// compute type, zero for blank slots (e >= card_j), padding dims and padding
+// sets.  rows[offsets[j] + e][d] holds set j's elements (storage dtype), so
+// the host only concatenates the sets -- no strided host transpose.
+template <int DT>
+__global__ void pack_elements_kernel(
+    const typename Traits<DT>::S *__restrict__ rows,
+    const int64_t *__restrict__ offsets, const int32_t *__restrict__ card,
+    int64_t l, int64_t l_pad, int k_max, int d, int d_pad,
+    typename Traits<DT>::C *__restrict__ packed) {
+  using C = typename Traits<DT>::C;
+  const int64_t j = (int64_t)blockIdx.x * 32 + threadIdx.x;
+  const int e = blockIdx.y;
+  if (j >= l_pad) return;
+  const bool live = j < l && e < card[j];
+  const int64_t base = live ? (offsets[j] + e) * (int64_t)d : 0;
+  const int64_t stride_k = (int64_t)k_max * l_pad;
+  for (int k = threadIdx.y; k < d_pad; k += blockDim.y) {
+    const C v = (live && k < d) ? to_c(rows[base + k]) : C(0);
+    packed[(int64_t)k * stride_k + (int64_t)e * l_pad + j] = v;
+  }
+}
+
 }  // namespace exem
 
 using namespace exem;
@@ -957,6 +981,26 @@ int exem_packed_norms(int dtype, const void *packed, int64_t d, int64_t k_max,
     packed_norms_kernel<float><<<grid, 256, 0, st>>>((const float *)packed,
                                                      (int)d, k_max, l_pad, out);
   EXEM_LAUNCH_CHECK("packed_norms_kernel");
+  return EXEM_OK;
+}
+
+int exem_pack_elements(int dtype, const void *rows, const int64_t *offsets,
+                       const int32_t *card, int64_t l, int64_t l_pad,
+                       int64_t k_max, int64_t d, void *packed, void *stream) {
+  if (l < 1 || k_max < 1 || d < 1 || l_pad < l || k_max > 65535)
+    return fail(EXEM_ERR_ARG, "pack_elements: bad shape");
+  const int d_pad = (int)exem_pad_dims(d);
+  dim3 block(32, 8);
+  dim3 grid((unsigned)ceil_div(l_pad, 32), (unsigned)k_max);
+  cudaStream_t st = (cudaStream_t)stream;
+  EXEM_DISPATCH(dtype, DT, {
+    using S = typename Traits<DT>::S;
+    using C = typename Traits<DT>::C;
+    pack_elements_kernel<DT><<<grid, block, 0, st>>>(
+        (const S *)rows, offsets, card, l, l_pad, (int)k_max, (int)d, d_pad,
+        (C *)packed);
+    EXEM_LAUNCH_CHECK("pack_elements_kernel");
+  });
   return EXEM_OK;
 }
 

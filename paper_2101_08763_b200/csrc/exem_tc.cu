@@ -160,9 +160,15 @@ __device__ __forceinline__ void mma_item_pipelined(
     if (t + 1 < ntiles) {  // acquire tile t+1 while tile t's tail is queued
       // (waiting earlier, e.g. after KS-4, was measured slower: tempty is
       // usually not yet released there)
+      if (p.trace != nullptr && blockIdx.x == 0 && s.tile_no + 1 < 256)
+        p.trace[0 * 256 + s.tile_no + 1] = clock64();
       mbar_wait(&tempty[nbuf], ((s.tph >> nbuf) & 1u) ^ 1u);
+      if (p.trace != nullptr && blockIdx.x == 0 && s.tile_no + 1 < 256)
+        p.trace[1 * 256 + s.tile_no + 1] = clock64();
       s.tph ^= 1u << nbuf;
       mbar_wait(&full[nstage], nph);
+      if (p.trace != nullptr && blockIdx.x == 0 && s.tile_no + 1 < 256)
+        p.trace[2 * 256 + s.tile_no + 1] = clock64();
       fence_after();
     }
     issue_range<H2, KS>(d, a_desc0, b0, p.idesc);
@@ -330,7 +336,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const int64_t p0 = sp * p.split_pts;
         const int64_t p1 = min(p.n, p0 + p.split_pts);
-        if (p.tile_stage && p.ksteps <= 8 && p.dbg == 0) {
+        if (p.tile_stage && p.ksteps <= 8 && (p.dbg & ~5) == 0) {
           // software-pipelined handshake (see mma_item_pipelined)
           const int ntiles = (int)((p1 - p0 + BN - 1) / BN);
           MmaState ms{stage, ph, tph, buf, tile_no};
@@ -352,7 +358,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tile_no = ms.tile_no;
         }
         for (int64_t pt = p0;
-             pt < p1 && !(p.tile_stage && p.ksteps <= 8 && p.dbg == 0);
+             pt < p1 && !(p.tile_stage && p.ksteps <= 8 && (p.dbg & ~5) == 0);
              pt += BN) {
           TR(0, tile_no);
           mbar_wait(&tempty[buf], ((tph >> buf) & 1u) ^ 1u);

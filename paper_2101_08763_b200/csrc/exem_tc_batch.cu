@@ -45,7 +45,6 @@ constexpr int A_CHUNK = BM * 128;       // bytes of one point K-chunk
 constexpr int kThreads = 320;
 constexpr int kEpiWarps = 8;
 constexpr int kMaxSpt = 32;             // sets per set tile (w >= 8)
-constexpr int kSetsPerWarp = kMaxSpt / 2;
 constexpr int kSmemBudget = 227 * 1024;
 constexpr int kBarBytes = 2048;
 
@@ -62,10 +61,170 @@ struct BParams {
   int kchunks;         // 64-wide K chunks per operand row
   int stages;          // point-chunk ring depth
   int bstream;         // 1: set chunks streamed with the point chunks
+  int dbg;             // timing experiments only (EXEM_TCB_DEBUG), 0 in use
   uint32_t idesc;
   const float *aux;    // [n] aux distances (compute type)
   double *partial;     // [splits][l]
 };
+
+__device__ __forceinline__ float max8(const uint32_t (&r)[8], float m) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) m = fmaxf(m, __uint_as_float(r[j]));
+  return m;
+}
+
+// Release an accumulator buffer: every lane's tcgen05.ld is complete.
+__device__ __forceinline__ void release_tmem(uint64_t *tempty_buf, int lane) {
+  fence_before();
+  __syncwarp();
+  if (lane == 0) mbar_arrive(tempty_buf);
+}
+
+// Epilogue of one accumulator tile for one warp, set width W8*8 columns known
+// at compile time.  The warp owns sets s = h + 2u (u < nsets); their columns
+// are drained with tcgen05.ld x8 into registers in batches of sets
+// (EpiShape) and ONE tcgen05.wait::ld per batch -- the TMEM load
+// latency is paid once per tile, not once per 32 columns -- and the buffer is
+// released right after the last batch's wait, before its arithmetic.
+//   t = min(aux_i, max(0, -2 max_e D)),  acc[u] += t   (fp64, per thread)
+template <int W8>
+struct EpiShape {
+  static constexpr int MAXS = (32 / W8 + 1) / 2;  // sets per warp (max)
+  // sets per load batch: registers of one batch (8 per group) plus the fp64
+  // accumulators within a 128-register budget (ptxas caps this kernel at
+  // 168 registers per thread)
+  static constexpr int sb() {
+    int best = 1;
+    for (int s = 1; s <= MAXS; ++s)
+      if (s * W8 * 8 + 2 * MAXS <= 128) best = s;
+    return best;
+  }
+  static constexpr int SB = sb();
+  static constexpr int NB = (MAXS + SB - 1) / SB;
+};
+
+template <int W8>
+__device__ __forceinline__ void epi_tile(
+    uint32_t taddr, int h, int spt, int w, float ax, bool valid,
+    double (&acc)[EpiShape<W8>::MAXS], uint64_t *tempty_buf, int lane) {
+  const float ninf = -__int_as_float(0x7f800000);
+  const int nsets = (spt - h + 1) >> 1;
+  if (nsets <= 0) {
+    release_tmem(tempty_buf, lane);
+    return;
+  }
+  if constexpr (W8 <= 16) {
+    constexpr int SB = EpiShape<W8>::SB;
+    constexpr int NB = EpiShape<W8>::NB;
+    const int nbat = (nsets + SB - 1) / SB;
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      if (b < nbat) {
+        uint32_t r[SB * W8][8];
+#pragma unroll
+        for (int j = 0; j < SB; ++j) {
+          if (b * SB + j < nsets) {
+            const uint32_t c0 = taddr + (uint32_t)((h + 2 * (b * SB + j)) * w);
+#pragma unroll
+            for (int g = 0; g < W8; ++g) TMEM_LD8(c0 + 8 * g, r[j * W8 + g]);
+          }
+        }
+        tmem_wait_ld();
+        if (b == nbat - 1) release_tmem(tempty_buf, lane);
+#pragma unroll
+        for (int j = 0; j < SB; ++j) {
+          if (b * SB + j < nsets) {
+            float mx = ninf;
+#pragma unroll
+            for (int g = 0; g < W8; ++g) mx = max8(r[j * W8 + g], mx);
+            const float t = fminf(ax, fmaxf(0.f, -2.f * mx));
+            if (valid) acc[b * SB + j] += (double)t;
+          }
+        }
+      }
+    }
+  } else {
+    // w > 128: one set per tile (spt == 1, only h == 0 has it); drain it in
+    // sub-batches of 16 groups with a running max
+    constexpr int NS = (W8 + 15) / 16;
+    float mx = ninf;
+#pragma unroll
+    for (int sb = 0; sb < NS; ++sb) {
+      uint32_t r[16][8];
+#pragma unroll
+      for (int g = 0; g < 16; ++g)
+        if (sb * 16 + g < W8) TMEM_LD8(taddr + 8 * (sb * 16 + g), r[g]);
+      tmem_wait_ld();
+      if (sb == NS - 1) release_tmem(tempty_buf, lane);
+#pragma unroll
+      for (int g = 0; g < 16; ++g)
+        if (sb * 16 + g < W8) mx = max8(r[g], mx);
+    }
+    const float t = fminf(ax, fmaxf(0.f, -2.f * mx));
+    if (valid) acc[0] += (double)t;
+  }
+}
+
+// The epilogue warps' whole loop for one set width (W8 = w/8 at compile
+// time, so the per-set column runs and the accumulator array are static).
+template <int W8>
+__device__ __forceinline__ void epilogue_role(const BParams &p, uint32_t tmem,
+                                              uint64_t *tfull,
+                                              uint64_t *tempty, double *red,
+                                              int warp, int lane,
+                                              int64_t items) {
+  constexpr int MAXS = EpiShape<W8>::MAXS;
+  const int ew = warp - 2;       // 0..7
+  const int q = warp & 3;        // TMEM lane quarter (lane access rule)
+  const int h = ew >> 2;         // set parity handled by this warp
+  const int row = q * 32 + lane; // point row within the tile
+  uint32_t buf = 0, tph = 0;
+  for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+    const int64_t st = it % p.set_tiles, sp = it / p.set_tiles;
+    const int64_t p0 = sp * p.split_pts;
+    const int64_t p1 = min(p.n, p0 + p.split_pts);
+    double acc[MAXS];
+#pragma unroll
+    for (int u = 0; u < MAXS; ++u) acc[u] = 0.0;
+    for (int64_t pt = p0; pt < p1; pt += BM) {
+      const int64_t pi = pt + row;
+      const bool valid = pi < p1;
+      const float ax = (valid && !(p.dbg & 8)) ? p.aux[pi] : 0.f;
+      if (lane == 0) mbar_wait_sleep(&tfull[buf], (tph >> buf) & 1u);
+      __syncwarp();
+      tph ^= 1u << buf;
+      fence_after();
+      const uint32_t taddr =
+          tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * 256);
+      if (p.dbg & 1)  // timing experiment: no TMEM drain / math
+        release_tmem(&tempty[buf], lane);
+      else
+        epi_tile<W8>(taddr, h, p.spt, p.w, ax, valid, acc, &tempty[buf], lane);
+      buf ^= 1u;
+    }
+    // item end: per set, fixed xor tree over the 32 lanes, then the four
+    // lane quarters in order
+#pragma unroll
+    for (int u = 0; u < MAXS; ++u) {
+      const int s = h + 2 * u;
+      if (s < p.spt) {
+        double v = acc[u];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) red[q * kMaxSpt + s] = v;
+      }
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+    if (ew == 0 && lane < p.spt) {
+      const int64_t j = st * p.spt + lane;
+      if (j < p.l)
+        p.partial[sp * p.l + j] =
+            ((red[lane] + red[kMaxSpt + lane]) + red[2 * kMaxSpt + lane]) +
+            red[3 * kMaxSpt + lane];
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+  }
+}
 
 __global__ void __launch_bounds__(kThreads, 1)
     batch_tc_kernel(const __grid_constant__ CUtensorMap map_p,
@@ -138,10 +297,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int kc = 0; kc < p.kchunks; ++kc) {
             mbar_wait_sleep(&empty[stage], ph ^ 1);
             unsigned char *dst = sa + stage * stage_bytes;
-            mbar_expect_tx(&full[stage], (uint32_t)stage_bytes);
-            tma_load_2d(dst, &map_p, &full[stage], kc * KCH, (int)pt);
-            if (p.bstream)
-              tma_load_2d(dst + A_CHUNK, &map_s, &full[stage], kc * KCH, srow);
+            if (p.dbg & 4) {  // timing experiment: no point-operand traffic
+              mbar_arrive(&full[stage]);
+            } else {
+              mbar_expect_tx(&full[stage], (uint32_t)stage_bytes);
+              tma_load_2d(dst, &map_p, &full[stage], kc * KCH, (int)pt);
+              if (p.bstream)
+                tma_load_2d(dst + A_CHUNK, &map_s, &full[stage], kc * KCH,
+                            srow);
+            }
             if (++stage == p.stages) {
               stage = 0;
               ph ^= 1;
@@ -191,7 +355,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             nph ^= 1u;
           }
 #pragma unroll 1
-          for (int j = 0; j < head; ++j)
+          for (int j = 0; j < head && !(p.dbg & 2); ++j)
             umma_f16(d, ad + (uint64_t)(2 * j), bd + (uint64_t)(2 * j),
                      p.idesc, (kc | j) ? 1u : 0u);
           if (e + 1 < nev) {  // acquire event e+1 behind the queued tail
@@ -204,7 +368,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             fence_after();
           }
 #pragma unroll 1
-          for (int j = head; j < nk; ++j)
+          for (int j = head; j < nk && !(p.dbg & 2); ++j)
             umma_f16(d, ad + (uint64_t)(2 * j), bd + (uint64_t)(2 * j),
                      p.idesc, (kc | j) ? 1u : 0u);
           umma_commit(&empty[stage]);
@@ -224,92 +388,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   } else {
     // -------------------------------------------------------------- epilogue
-    const int ew = warp - 2;       // 0..7
-    const int q = warp & 3;        // TMEM lane quarter
-    const int h = ew >> 2;         // set parity handled by this warp
-    const int row = q * 32 + lane; // point row within the tile
-    const int w8 = p.w >> 3;
-    uint32_t buf = 0, tph = 0;
-    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
-      const int64_t st = it % p.set_tiles, sp = it / p.set_tiles;
-      const int64_t p0 = sp * p.split_pts;
-      const int64_t p1 = min(p.n, p0 + p.split_pts);
-      double acc[kSetsPerWarp];
-#pragma unroll
-      for (int u = 0; u < kSetsPerWarp; ++u) acc[u] = 0.0;
-      for (int64_t pt = p0; pt < p1; pt += BM) {
-        const int64_t pi = pt + row;
-        const bool valid = pi < p1;
-        const float ax = valid ? p.aux[pi] : 0.f;
-        if (lane == 0) mbar_wait_sleep(&tfull[buf], (tph >> buf) & 1u);
-        __syncwarp();
-        tph ^= 1u << buf;
-        fence_after();
-        const uint32_t taddr =
-            tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * 256);
-#pragma unroll
-        for (int u = 0; u < kSetsPerWarp; ++u) {
-          const int s = h + 2 * u;
-          if (s < p.spt) {  // warp-uniform
-            const uint32_t c0 = taddr + (uint32_t)(s * p.w);
-            float mx = -__int_as_float(0x7f800000);
-            for (int g = 0; g < w8; g += 4) {
-              uint32_t r[32];
-              TMEM_LD8(c0 + g * 8, r);
-              if (g + 1 < w8) TMEM_LD8(c0 + g * 8 + 8, r + 8);
-              if (g + 2 < w8) TMEM_LD8(c0 + g * 8 + 16, r + 16);
-              if (g + 3 < w8) TMEM_LD8(c0 + g * 8 + 24, r + 24);
-              tmem_wait_ld();
-#pragma unroll
-              for (int j = 0; j < 8; ++j) mx = fmaxf(mx, __uint_as_float(r[j]));
-              if (g + 1 < w8) {
-#pragma unroll
-                for (int j = 8; j < 16; ++j)
-                  mx = fmaxf(mx, __uint_as_float(r[j]));
-              }
-              if (g + 2 < w8) {
-#pragma unroll
-                for (int j = 16; j < 24; ++j)
-                  mx = fmaxf(mx, __uint_as_float(r[j]));
-              }
-              if (g + 3 < w8) {
-#pragma unroll
-                for (int j = 24; j < 32; ++j)
-                  mx = fmaxf(mx, __uint_as_float(r[j]));
-              }
-            }
-            // t_i = min(aux_i, max(0, min_e d)), min_e d = -2 max_e D
-            const float t = fminf(ax, fmaxf(0.f, -2.f * mx));
-            if (valid) acc[u] += (double)t;
-          }
-        }
-        fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[buf]);
-        buf ^= 1u;
-      }
-      // item end: per set, fixed xor tree over the 32 lanes, then the four
-      // lane quarters in order
-#pragma unroll
-      for (int u = 0; u < kSetsPerWarp; ++u) {
-        const int s = h + 2 * u;
-        if (s < p.spt) {
-          double v = acc[u];
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1)
-            v += __shfl_xor_sync(0xffffffffu, v, o);
-          if (lane == 0) red[q * kMaxSpt + s] = v;
-        }
-      }
-      asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
-      if (ew == 0 && lane < p.spt) {
-        const int64_t j = st * p.spt + lane;
-        if (j < p.l)
-          p.partial[sp * p.l + j] =
-              ((red[lane] + red[kMaxSpt + lane]) + red[2 * kMaxSpt + lane]) +
-              red[3 * kMaxSpt + lane];
-      }
-      asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+    switch (p.w >> 3) {
+#define EXEM_EPI_CASE(W) \
+  case W: epilogue_role<W>(p, tmem, tfull, tempty, red, warp, lane, items); break;
+      EXEM_EPI_CASE(1) EXEM_EPI_CASE(2) EXEM_EPI_CASE(3) EXEM_EPI_CASE(4)
+      EXEM_EPI_CASE(5) EXEM_EPI_CASE(6) EXEM_EPI_CASE(7) EXEM_EPI_CASE(8)
+      EXEM_EPI_CASE(9) EXEM_EPI_CASE(10) EXEM_EPI_CASE(11) EXEM_EPI_CASE(12)
+      EXEM_EPI_CASE(13) EXEM_EPI_CASE(14) EXEM_EPI_CASE(15) EXEM_EPI_CASE(16)
+      EXEM_EPI_CASE(17) EXEM_EPI_CASE(18) EXEM_EPI_CASE(19) EXEM_EPI_CASE(20)
+      EXEM_EPI_CASE(21) EXEM_EPI_CASE(22) EXEM_EPI_CASE(23) EXEM_EPI_CASE(24)
+      EXEM_EPI_CASE(25) EXEM_EPI_CASE(26) EXEM_EPI_CASE(27) EXEM_EPI_CASE(28)
+      EXEM_EPI_CASE(29) EXEM_EPI_CASE(30) EXEM_EPI_CASE(31) EXEM_EPI_CASE(32)
+#undef EXEM_EPI_CASE
+      default: break;
     }
   }
 
@@ -455,6 +546,10 @@ int exem_batch_eval_tc(int dtype, const void *xp, int64_t n, const void *aux,
   prm.kchunks = (int)(kp / KCH);
   prm.idesc = make_idesc(dtype == EXEM_BF16, BM, nc);
   prm.aux = (const float *)aux;
+  {
+    const char *dbg = getenv("EXEM_TCB_DEBUG");
+    prm.dbg = dbg ? atoi(dbg) : 0;
+  }
   prm.partial = partial;
   const int b_chunk = nc * 128;
   const int avail = kSmemBudget - kBarBytes - 1024;

@@ -171,7 +171,6 @@ def sharded_batch_sums(ground, batch, rank: int, world: int, group=None,
     import torch.distributed as dist
 
     from . import _native as N
-    from .core import pack_batch
     from .streaming import stream_packed_sums
 
     lib = N.lib()
@@ -179,24 +178,23 @@ def sharded_batch_sums(ground, batch, rank: int, world: int, group=None,
     sp = int(lib.split_points(n))
     splits = -(-n // sp)
     r0, r1 = shard_rows(n, world, rank, sp)
-    packed = pack_batch(batch, ground.precision)
     dev = torch.device("cuda", torch.cuda.current_device()
                        if device is None else device)
-    partial = torch.zeros((splits, packed.l), dtype=torch.float64, device=dev)
+    partial = torch.zeros((splits, batch.l), dtype=torch.float64, device=dev)
     if budget is None:
         budget = ground.device_budget or int(
             0.8 * torch.cuda.mem_get_info(dev)[0])
     if r1 > r0:
-        stream_packed_sums(ground, packed.values, packed.d, packed.k_max,
-                           packed.l, packed.cardinalities, dev.index,
-                           rows=(r0, r1), partial=partial, budget=budget)
+        stream_packed_sums(ground, None, batch.d, batch.k_max, batch.l,
+                           batch.cardinalities, dev.index, rows=(r0, r1),
+                           partial=partial, budget=budget, sets=batch.sets)
 
     def all_reduce(t):
         if world > 1 and dist.is_available() and dist.is_initialized():
             dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
 
     combine_partials(partial, all_reduce)
-    sums = torch.empty(packed.l, dtype=torch.float64, device=dev)
-    lib.reduce_partials(N.ptr(partial), splits, packed.l, 1.0, N.ptr(sums),
+    sums = torch.empty(batch.l, dtype=torch.float64, device=dev)
+    lib.reduce_partials(N.ptr(partial), splits, batch.l, 1.0, N.ptr(sums),
                         N.stream_handle(dev))
     return sums

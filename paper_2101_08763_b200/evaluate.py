@@ -143,21 +143,40 @@ class DeviceBatch:
     plus what the batch kernels need: element norms, cardinalities and, for
     half precision, the K4-TC set-tile operand."""
 
-    def __init__(self, values: np.ndarray, d: int, k_max: int, l: int,
-                 cardinalities, precision: Precision, d_pad: int, dev,
-                 stream):
-        from .device import torch
+    def __init__(self, values: Optional[np.ndarray], d: int, k_max: int,
+                 l: int, cardinalities, precision: Precision, d_pad: int, dev,
+                 stream, sets=None):
+        """``values``: a packed (d, k_max, l) host buffer (PackedBatch), or
+        None with ``sets`` = the l element arrays, which are concatenated on
+        the host and interleaved on the device (exem_pack_elements)."""
+        from .device import to_device_bytes, torch
 
         t = torch()
         lib = N.lib()
         self.d, self.k_max, self.l = d, k_max, l
         self.l_pad = int(-(-l // 128) * 128)
         self.precision = precision
-        host = np.zeros((d_pad, k_max, self.l_pad),
-                        dtype=precision.compute_dtype)
-        host[:d, :, :l] = np.asarray(values, dtype=precision.dtype).reshape(
-            d, k_max, l).astype(precision.compute_dtype)
-        self.packed = t.from_numpy(host).to(dev)
+        cdt = t.float64 if precision.compute_dtype == np.float64 else t.float32
+        if sets is not None:
+            rows = np.concatenate([np.asarray(x, dtype=precision.dtype)
+                                   .reshape(-1, d) for x in sets])
+            cards = np.asarray(cardinalities, dtype=np.int64)
+            offsets = np.zeros(l, dtype=np.int64)
+            np.cumsum(cards[:-1], out=offsets[1:])
+            rows_d = to_device_bytes(rows, dev)
+            offs_d = t.from_numpy(offsets).to(dev)
+            card_d = t.from_numpy(cards.astype(np.int32)).to(dev)
+            self.packed = t.empty((d_pad, k_max, self.l_pad), dtype=cdt,
+                                  device=dev)
+            lib.pack_elements(precision.tag, N.ptr(rows_d), N.ptr(offs_d),
+                              N.ptr(card_d), l, self.l_pad, k_max, d,
+                              N.ptr(self.packed), stream)
+        else:
+            host = np.zeros((d_pad, k_max, self.l_pad),
+                            dtype=precision.compute_dtype)
+            host[:d, :, :l] = np.asarray(values, dtype=precision.dtype).reshape(
+                d, k_max, l).astype(precision.compute_dtype)
+            self.packed = t.from_numpy(host).to(dev)
         self.pnorms = t.empty((k_max, self.l_pad), dtype=t.float64, device=dev)
         lib.packed_norms(precision.tag, N.ptr(self.packed), d, k_max,
                          self.l_pad, N.ptr(self.pnorms), stream)
@@ -193,9 +212,11 @@ def batch_partials(dg, batch: DeviceBatch, partial, split_pts: int,
                        dg.stream)
 
 
-def device_packed_sums(ground: GroundSet, values: np.ndarray, d: int,
-                       k_max: int, l: int, cardinalities, device=None):
-    """Upload a packed (d, k_max, l) buffer and run K4 (or K4-TC) + K6.
+def device_packed_sums(ground: GroundSet, values: Optional[np.ndarray],
+                       d: int, k_max: int, l: int, cardinalities, device=None,
+                       sets=None):
+    """Upload a batch -- a packed (d, k_max, l) buffer, or the sets' element
+    arrays -- and run K4 (or K4-TC) + K6.
 
     Returns the device tensor of per-set fp64 sums sum_i t_i(S_j).
     """
@@ -205,14 +226,14 @@ def device_packed_sums(ground: GroundSet, values: np.ndarray, d: int,
         from .streaming import stream_packed_sums
 
         return stream_packed_sums(ground, values, d, k_max, l, cardinalities,
-                                  device)
+                                  device, sets=sets)
     t = torch()
     lib = N.lib()
     dg = ground.on_device(device)
     with t.cuda.device(dg.device_index):
         st = dg.stream
         batch = DeviceBatch(values, d, k_max, l, cardinalities,
-                            ground.precision, dg.d_pad, dg.dev, st)
+                            ground.precision, dg.d_pad, dg.dev, st, sets=sets)
         partial = t.empty((dg.splits, l), dtype=t.float64, device=dg.dev)
         batch_partials(dg, batch, partial, dg.split_pts, dg.splits)
         sums = t.empty(l, dtype=t.float64, device=dg.dev)
@@ -251,10 +272,10 @@ def evaluate_batch(evaluator: Evaluator, ground: GroundSet,
     """One value per set (evaluate.py:273-293) -- kernels K4 + K6."""
     require_device_dissimilarity(dissimilarity)
     _check_batch(ground, batch)
-    precision = _effective_precision(evaluator, ground)
-    packed = pack_batch(batch, precision)
-    sums = device_packed_sums(ground, packed.values, packed.d, packed.k_max,
-                              packed.l, packed.cardinalities, evaluator.device)
+    _effective_precision(evaluator, ground)
+    sums = device_packed_sums(ground, None, batch.d, batch.k_max, batch.l,
+                              batch.cardinalities, evaluator.device,
+                              sets=batch.sets)
     return _finish(ground, sums.cpu().numpy())
 
 

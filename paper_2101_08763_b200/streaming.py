@@ -318,7 +318,8 @@ def batch_device_bytes(d: int, k_max: int, l: int, precision,
 
 
 def stream_packed_sums(ground, values, d, k_max, l, cardinalities,
-                       device=None, rows=None, partial=None, budget=None):
+                       device=None, rows=None, partial=None, budget=None,
+                       sets=None):
     """Streamed K4 / K4-TC: per-set fp64 sums over the rows [row0, row1)
     (all rows by default).  With ``partial`` given (a [splits][l] fp64
     device tensor), the per-split partials are written there at their
@@ -340,7 +341,7 @@ def stream_packed_sums(ground, values, d, k_max, l, cardinalities,
         with t.cuda.device(gs.idx):
             st = N.stream_handle(gs.dev)
             batch = DeviceBatch(values, d, k_max, l, cardinalities, prec,
-                                int(lib.pad_dims(d)), gs.dev, st)
+                                int(lib.pad_dims(d)), gs.dev, st, sets=sets)
             own = partial is None
             if own:
                 partial = t.zeros((splits, l), dtype=t.float64, device=gs.dev)

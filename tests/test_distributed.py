@@ -120,3 +120,59 @@ def test_shard_rows_partition():
                 assert a1 % sp == 0 or a1 == n
     with pytest.raises(ValueError):
         shard_rows(10, 2, 2, 1024)
+
+
+# ------------------------------------------------------------ explicit batches
+def _split_partials(V, sets, rows, split_pts):
+    """[splits][l] fp64 partials of t_i(S_j) over this rank's rows only."""
+    n = V.shape[0]
+    splits = -(-n // split_pts)
+    aux = O.aux64(V)
+    out = np.zeros((splits, len(sets)))
+    r0, r1 = rows
+    for j, S in enumerate(sets):
+        d = ((V[r0:r1, None, :] - V[S][None, :, :]) ** 2).sum(-1).min(1)
+        t = np.minimum(aux[r0:r1], d)
+        for s in range(r0 // split_pts, -(-r1 // split_pts)):
+            a, b = max(r0, s * split_pts), min(r1, (s + 1) * split_pts)
+            out[s, j] = t[a - r0:b - r0].sum()
+    return out
+
+
+def _batch_worker(rank, world, port, V, sets, split_pts, out):
+    from paper_2101_08763_b200.distributed import combine_partials
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rows = shard_rows(V.shape[0], world, rank, split_pts)
+        part = torch.from_numpy(_split_partials(V, sets, rows, split_pts))
+
+        def all_reduce(t):
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+
+        combine_partials(part, all_reduce)
+        out[rank] = part.numpy()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_batch_partials_exact(world):
+    """Config 5's collective: each rank fills its own split rows of the
+    [splits][l] matrix, the all-reduce of the zero-padded matrices equals the
+    single-process matrix BIT FOR BIT (x + 0 is exact), so the fixed-order
+    per-set reduction that follows is independent of the rank count."""
+    rng = np.random.default_rng(world)
+    n, d, split_pts = 5000, 6, 1024
+    V = rng.standard_normal((n, d))
+    sets = [rng.choice(n, size=int(rng.integers(1, 6)), replace=False)
+            for _ in range(7)]
+    ref = _split_partials(V, sets, (0, n), split_pts)
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_batch_worker, args=(world, _free_port(), V, sets, split_pts, out),
+             nprocs=world, join=True)
+    for rank in range(world):
+        assert np.array_equal(out[rank], ref)

@@ -256,3 +256,46 @@ def test_product_never_imports_oracle():
         text = py.read_text()
         assert "exem_oracle" not in text and "import oracle" not in text, py
         assert "from oracle" not in text, py
+
+
+def test_stream_plan_is_split_aligned(native_lib):
+    """Low-memory regime planning (streaming.py): slices are whole
+    partial-sum splits covering [0, n) in order, sized so two ring slots fit
+    the budget; below one split per slot -> OutOfMemoryError."""
+    from paper_2101_08763_b200 import streaming as S
+
+    P = pb.Precision
+    for n, d, prec in ((20_000, 37, P.binary32), (1_000_000, 100, P.bfloat16),
+                       (50_000_000, 256, P.bfloat16), (5000, 8, P.binary64)):
+        sp = int(native_lib.split_points(n))
+        one = S.layout_bytes(sp, d, prec, with_src=True)
+        for budget in (2 * one, 5 * one + 17, 40 * one):
+            plan = S.plan_slices(n, d, prec, budget, sp)
+            assert plan.slices[0][0] == 0 and plan.slices[-1][1] == n
+            for (a0, a1), (b0, b1) in zip(plan.slices, plan.slices[1:]):
+                assert a1 == b0 and a1 % sp == 0
+            assert 2 * plan.slot_bytes <= budget
+            assert plan.rows_per_slice % sp == 0 or plan.rows_per_slice == n
+        with pytest.raises(pb.OutOfMemoryError):
+            S.plan_slices(n, d, prec, 2 * one - 1, sp)
+        assert S.resident_bytes(n, d, prec) > S.layout_bytes(n, d, prec)
+        assert S.fits_resident(n, d, prec, None)
+        assert not S.fits_resident(n, d, prec, S.resident_bytes(n, d, prec) - 1)
+
+
+def test_tc_set_geometry(native_lib):
+    """K4-TC set tiles: w = round_up(k_max, 8) columns per set, as many whole
+    sets as fit 256 TMEM columns (<= 32), MMA N a multiple of 16."""
+    import ctypes
+
+    geo = native_lib.raw("exem_tc_set_geometry")
+    for k in (1, 7, 8, 9, 50, 128, 129, 256):
+        spt, w, nc = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        assert geo(k, ctypes.byref(spt), ctypes.byref(w), ctypes.byref(nc)) == 0
+        assert w.value == -(-k // 8) * 8
+        assert spt.value == min(32, 256 // w.value)
+        assert nc.value % 16 == 0 and spt.value * w.value <= nc.value <= 256
+        rows = native_lib.tc_set_rows(1000, k)
+        assert rows == -(-1000 // spt.value) * nc.value
+    spt, w, nc = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    assert geo(257, ctypes.byref(spt), ctypes.byref(w), ctypes.byref(nc)) == 5
