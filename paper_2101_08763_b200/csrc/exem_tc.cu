@@ -130,18 +130,21 @@ struct MmaState {
   int tile_no;
 };
 
+
 // One work item (a split's point tiles against the stationary candidate
-// tile) with a software-pipelined handshake: the barrier waits for tile t+1
-// (accumulator buffer free, B stage landed) are placed between tile t's last
-// two MMAs, so their latency (~100-200 cycles each) hides behind queued
-// tensor work instead of opening a bubble in the ~2-deep MMA queue.
-template <int KS, typename P>
-__device__ __forceinline__ void mma_item_pipelined(
+// tile) with a software-pipelined handshake: the two acquisitions for tile
+// t+1 -- B stage landed (full) and accumulator buffer free (tempty) -- are
+// placed before MMA index WF / WT of tile t, so their latency hides behind
+// queued tensor work instead of opening a bubble in the ~2-deep MMA queue.
+// Index KS = after the whole tile (and its commits).  Measured at C4
+// (tools/k3_waits.sh, profiles/r01_k3_waits.log): WF = KS-2, WT = KS-1 is
+// 6 % faster than both before KS-2 (185.4 -> 173.5 ms); waiting for tempty
+// after the tile costs 25 %.
+template <int KS, int WF, int WT, typename P>
+__device__ __forceinline__ void mma_item_waits(
     const P &p, int ntiles, MmaState &s, uint64_t a_desc0, uint64_t b_desc0,
     uint32_t stage_step, uint32_t tmem, uint64_t *full, uint64_t *empty,
     uint64_t *tfull, uint64_t *tempty) {
-  constexpr int H2 = KS > 2 ? KS - 2 : 0;
-  // acquire tile 0 of the item
   mbar_wait(&tempty[s.buf], ((s.tph >> s.buf) & 1u) ^ 1u);
   s.tph ^= 1u << s.buf;
   mbar_wait(&full[s.stage], s.ph);
@@ -156,26 +159,34 @@ __device__ __forceinline__ void mma_item_pipelined(
       nstage = 0;
       nph ^= 1u;
     }
-    issue_range<0, H2>(d, a_desc0, b0, p.idesc);
-    if (t + 1 < ntiles) {  // acquire tile t+1 while tile t's tail is queued
-      // (waiting earlier, e.g. after KS-4, was measured slower: tempty is
-      // usually not yet released there)
-      if (p.trace != nullptr && blockIdx.x == 0 && s.tile_no + 1 < 256)
-        p.trace[0 * 256 + s.tile_no + 1] = clock64();
-      mbar_wait(&tempty[nbuf], ((s.tph >> nbuf) & 1u) ^ 1u);
-      if (p.trace != nullptr && blockIdx.x == 0 && s.tile_no + 1 < 256)
-        p.trace[1 * 256 + s.tile_no + 1] = clock64();
-      s.tph ^= 1u << nbuf;
-      mbar_wait(&full[nstage], nph);
-      if (p.trace != nullptr && blockIdx.x == 0 && s.tile_no + 1 < 256)
-        p.trace[2 * 256 + s.tile_no + 1] = clock64();
-      fence_after();
+    const bool more = t + 1 < ntiles;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      if (ks == WT && more) {
+        mbar_wait(&tempty[nbuf], ((s.tph >> nbuf) & 1u) ^ 1u);
+        s.tph ^= 1u << nbuf;
+        fence_after();
+      }
+      if (ks == WF && more) {
+        mbar_wait(&full[nstage], nph);
+        fence_after();
+      }
+      constexpr uint32_t kA = 128 * 128 >> 4, kB = 256 * 128 >> 4;
+      umma_f16(d, a_desc0 + (uint64_t)((ks >> 2) * kA + (ks & 3) * 2),
+               b0 + (uint64_t)((ks >> 2) * kB + (ks & 3) * 2), p.idesc,
+               ks > 0 ? 1u : 0u);
     }
-    issue_range<H2, KS>(d, a_desc0, b0, p.idesc);
     umma_commit(&empty[s.stage]);
     umma_commit(&tfull[s.buf]);
-    if (p.trace != nullptr && blockIdx.x == 0 && s.tile_no < 256)
-      p.trace[3 * 256 + s.tile_no] = clock64();
+    if (WT == KS && more) {
+      mbar_wait(&tempty[nbuf], ((s.tph >> nbuf) & 1u) ^ 1u);
+      s.tph ^= 1u << nbuf;
+      fence_after();
+    }
+    if (WF == KS && more) {
+      mbar_wait(&full[nstage], nph);
+      fence_after();
+    }
     ++s.tile_no;
     s.buf = nbuf;
     s.stage = nstage;
@@ -212,6 +223,7 @@ struct Params {
   int kchunks;          // 64-wide K chunks loaded per operand tile
   int stages;           // B pipeline depth (in K chunks)
   int dbg;              // timing experiments only (EXEM_TC_DEBUG), 0 in use
+  int wait_mode;        // timing experiments: 8 = epilogue spins on tfull (EXEM_TC_WAITS)
   int tile_stage;       // 1: a pipeline stage holds a whole B tile
   uint32_t idesc;
   double *partial;
@@ -337,19 +349,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int64_t p0 = sp * p.split_pts;
         const int64_t p1 = min(p.n, p0 + p.split_pts);
         if (p.tile_stage && p.ksteps <= 8 && (p.dbg & ~5) == 0) {
-          // software-pipelined handshake (see mma_item_pipelined)
+          // software-pipelined handshake (see mma_item_waits)
           const int ntiles = (int)((p1 - p0 + BN - 1) / BN);
           MmaState ms{stage, ph, tph, buf, tile_no};
           const uint32_t st_step = stage_step;
           switch (p.ksteps) {
-            case 1: mma_item_pipelined<1>(p, ntiles, ms, a_desc0, b_desc0, st_step, tmem, full, empty, tfull, tempty); break;
-            case 2: mma_item_pipelined<2>(p, ntiles, ms, a_desc0, b_desc0, st_step, tmem, full, empty, tfull, tempty); break;
-            case 3: mma_item_pipelined<3>(p, ntiles, ms, a_desc0, b_desc0, st_step, tmem, full, empty, tfull, tempty); break;
-            case 4: mma_item_pipelined<4>(p, ntiles, ms, a_desc0, b_desc0, st_step, tmem, full, empty, tfull, tempty); break;
-            case 5: mma_item_pipelined<5>(p, ntiles, ms, a_desc0, b_desc0, st_step, tmem, full, empty, tfull, tempty); break;
-            case 6: mma_item_pipelined<6>(p, ntiles, ms, a_desc0, b_desc0, st_step, tmem, full, empty, tfull, tempty); break;
-            case 7: mma_item_pipelined<7>(p, ntiles, ms, a_desc0, b_desc0, st_step, tmem, full, empty, tfull, tempty); break;
-            default: mma_item_pipelined<8>(p, ntiles, ms, a_desc0, b_desc0, st_step, tmem, full, empty, tfull, tempty); break;
+#define EXEM_K3_ITEM(K)                                                       \
+  case K:                                                                     \
+    mma_item_waits<K, (K > 2 ? K - 2 : 0), (K > 1 ? K - 1 : 0)>(             \
+        p, ntiles, ms, a_desc0, b_desc0, st_step, tmem, full, empty, tfull,   \
+        tempty);                                                              \
+    break;
+            EXEM_K3_ITEM(1) EXEM_K3_ITEM(2) EXEM_K3_ITEM(3) EXEM_K3_ITEM(4)
+            EXEM_K3_ITEM(5) EXEM_K3_ITEM(6) EXEM_K3_ITEM(7)
+            default: EXEM_K3_ITEM(8)
+#undef EXEM_K3_ITEM
           }
           stage = ms.stage;
           ph = ms.ph;
@@ -445,7 +459,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int64_t pt = p0; pt < p1; pt += BN) {
         if (tr) TR(4, tile_no);
         // one lane polls the barrier; the warp sync orders the others
-        if (lane == 0) mbar_wait_sleep(&tfull[buf], (tph >> buf) & 1u);
+        if (lane == 0) {
+          if (p.wait_mode & 8)
+            mbar_wait(&tfull[buf], (tph >> buf) & 1u);
+          else
+            mbar_wait_sleep(&tfull[buf], (tph >> buf) & 1u);
+        }
         __syncwarp();
         if (tr) TR(5, tile_no);
         tph ^= 1u << buf;
@@ -641,6 +660,8 @@ int exem_greedy_gains_tc(int dtype, const void *xc, int64_t l, const void *xp,
   {
     const char *dbg = getenv("EXEM_TC_DEBUG");
     prm.dbg = dbg ? atoi(dbg) : 0;
+    const char *wm = getenv("EXEM_TC_WAITS");
+    prm.wait_mode = wm ? atoi(wm) : 0;
   }
   prm.trace = nullptr;
   const char *trace_path = getenv("EXEM_TC_TRACE");

@@ -346,8 +346,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                                         : b_base + (uint64_t)(kc * b_step);
           const int rem = p.ksteps - kc * 4;
           const int nk = rem < 4 ? rem : 4;
-          const int head = nk > 2 ? nk - 2 : 0;
+          // acquisitions for event e+1 (accumulator buffer when e+1 starts a
+          // tile, then its point chunk) hide behind this chunk's last two
+          // queued MMAs.  (Splitting them -- B stage before MMA nk-2, buffer
+          // before nk-1, the better placement for K3 -- measured 1.5x
+          // slower here: profiles/r01_k4_probe.log.)
+          const int wf = nk > 2 ? nk - 2 : 0;
+          const int wt = wf;
           const bool last = (kc == p.kchunks - 1);
+          const bool more = e + 1 < nev;
           int nstage = stage + 1;
           uint32_t nph = ph;
           if (nstage == p.stages) {
@@ -355,22 +362,21 @@ __global__ void __launch_bounds__(kThreads, 1)
             nph ^= 1u;
           }
 #pragma unroll 1
-          for (int j = 0; j < head && !(p.dbg & 2); ++j)
-            umma_f16(d, ad + (uint64_t)(2 * j), bd + (uint64_t)(2 * j),
-                     p.idesc, (kc | j) ? 1u : 0u);
-          if (e + 1 < nev) {  // acquire event e+1 behind the queued tail
-            if (last) {
+          for (int j = 0; j < nk; ++j) {
+            if (more && last && j == wt) {
               const uint32_t nb = buf ^ 1u;
               mbar_wait(&tempty[nb], ((tph >> nb) & 1u) ^ 1u);
               tph ^= 1u << nb;
+              fence_after();
             }
-            mbar_wait(&full[nstage], nph);
-            fence_after();
+            if (more && j == wf) {
+              mbar_wait(&full[nstage], nph);
+              fence_after();
+            }
+            if (!(p.dbg & 2))
+              umma_f16(d, ad + (uint64_t)(2 * j), bd + (uint64_t)(2 * j),
+                       p.idesc, (kc | j) ? 1u : 0u);
           }
-#pragma unroll 1
-          for (int j = head; j < nk && !(p.dbg & 2); ++j)
-            umma_f16(d, ad + (uint64_t)(2 * j), bd + (uint64_t)(2 * j),
-                     p.idesc, (kc | j) ? 1u : 0u);
           umma_commit(&empty[stage]);
           if (last) {
             umma_commit(&tfull[buf]);

@@ -540,8 +540,17 @@ int run_pp(const char *name, int tiles) {
   return 0;
 }
 
-int main() {
+int main(int argc, char **argv) {
   const int T = 4000, K = 7;
+  if (argc > 1) {  // cta_group::2 shapes only
+    int dm = 1;
+    cudaMemcpyToSymbol(g_data, &dm, sizeof(int));
+    run<128, 256, 1, false>("cg1 M128 N256", T, K);
+    run<256, 256, 2, false>("cg2 M256 N256", T, K);
+    run<256, 128, 2, false>("cg2 M256 N128", 2 * T, K);
+    run<256, 256, 2, true>("cg2 M256 N256 +ldtm", T, K);
+    return 0;
+  }
   for (int dm = 0; dm < 3; ++dm) {
     cudaMemcpyToSymbol(g_data, &dm, sizeof(int));
     printf("--- operand data mode %d (0 small-positive, 1 gaussian-like, 2 zeros)\n", dm);
