@@ -73,12 +73,23 @@ __device__ __forceinline__ float max8(const uint32_t (&r)[8], float m) {
   return m;
 }
 
-// Release an accumulator buffer: every lane's tcgen05.ld is complete.
-__device__ __forceinline__ void release_tmem(uint64_t *tempty_buf, int lane) {
-  fence_before();
-  __syncwarp();
-  if (lane == 0) mbar_arrive(tempty_buf);
-}
+// Release an accumulator buffer once every lane's tcgen05.ld is complete:
+// on this CTA's tempty (CG = 1) or on the pair leader's (CG = 2).
+template <int CG>
+struct TmemRelease {
+  uint64_t *bar;
+  int lane;
+  __device__ __forceinline__ void operator()() const {
+    fence_before();
+    __syncwarp();
+    if (lane == 0) {
+      if constexpr (CG == 2)
+        mbar_arrive_cluster(mapa(bar, 0));
+      else
+        mbar_arrive(bar);
+    }
+  }
+};
 
 // Epilogue of one accumulator tile for one warp, set width W8*8 columns known
 // at compile time.  The warp owns sets s = h + 2u (u < nsets); their columns
@@ -103,14 +114,14 @@ struct EpiShape {
   static constexpr int NB = (MAXS + SB - 1) / SB;
 };
 
-template <int W8>
+template <int W8, typename Release>
 __device__ __forceinline__ void epi_tile(
     uint32_t taddr, int h, int spt, int w, float ax, bool valid,
-    double (&acc)[EpiShape<W8>::MAXS], uint64_t *tempty_buf, int lane) {
+    double (&acc)[EpiShape<W8>::MAXS], const Release &release) {
   const float ninf = -__int_as_float(0x7f800000);
   const int nsets = (spt - h + 1) >> 1;
   if (nsets <= 0) {
-    release_tmem(tempty_buf, lane);
+    release();
     return;
   }
   if constexpr (W8 <= 16) {
@@ -130,7 +141,7 @@ __device__ __forceinline__ void epi_tile(
           }
         }
         tmem_wait_ld();
-        if (b == nbat - 1) release_tmem(tempty_buf, lane);
+        if (b == nbat - 1) release();
 #pragma unroll
         for (int j = 0; j < SB; ++j) {
           if (b * SB + j < nsets) {
@@ -155,7 +166,7 @@ __device__ __forceinline__ void epi_tile(
       for (int g = 0; g < 16; ++g)
         if (sb * 16 + g < W8) TMEM_LD8(taddr + 8 * (sb * 16 + g), r[g]);
       tmem_wait_ld();
-      if (sb == NS - 1) release_tmem(tempty_buf, lane);
+      if (sb == NS - 1) release();
 #pragma unroll
       for (int g = 0; g < 16; ++g)
         if (sb * 16 + g < W8) mx = max8(r[g], mx);
@@ -167,27 +178,34 @@ __device__ __forceinline__ void epi_tile(
 
 // The epilogue warps' whole loop for one set width (W8 = w/8 at compile
 // time, so the per-set column runs and the accumulator array are static).
-template <int W8>
+// CG = 2: this CTA holds rows [128*rank, 128*rank+128) of each 256-point
+// pair tile; buffers are released on the leader's tempty, and at item end
+// the peer's per-set sums travel to the leader through DSMEM (xbuf) so the
+// leader writes one fixed-order partial per (split, set).
+template <int CG, int W8>
 __device__ __forceinline__ void epilogue_role(const BParams &p, uint32_t tmem,
                                               uint64_t *tfull,
                                               uint64_t *tempty, double *red,
-                                              int warp, int lane,
-                                              int64_t items) {
+                                              double *xbuf, uint64_t *xfull,
+                                              uint64_t *xempty, int warp,
+                                              int lane, int64_t items,
+                                              uint32_t rank, int64_t pair,
+                                              int64_t npairs) {
   constexpr int MAXS = EpiShape<W8>::MAXS;
   const int ew = warp - 2;       // 0..7
   const int q = warp & 3;        // TMEM lane quarter (lane access rule)
   const int h = ew >> 2;         // set parity handled by this warp
-  const int row = q * 32 + lane; // point row within the tile
-  uint32_t buf = 0, tph = 0;
-  for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+  const int row = q * 32 + lane; // point row within this CTA's tile half
+  uint32_t buf = 0, tph = 0, xph = 0;
+  for (int64_t it = pair; it < items; it += npairs) {
     const int64_t st = it % p.set_tiles, sp = it / p.set_tiles;
     const int64_t p0 = sp * p.split_pts;
     const int64_t p1 = min(p.n, p0 + p.split_pts);
     double acc[MAXS];
 #pragma unroll
     for (int u = 0; u < MAXS; ++u) acc[u] = 0.0;
-    for (int64_t pt = p0; pt < p1; pt += BM) {
-      const int64_t pi = pt + row;
+    for (int64_t pt = p0; pt < p1; pt += BM * CG) {
+      const int64_t pi = pt + BM * rank + row;
       const bool valid = pi < p1;
       const float ax = (valid && !(p.dbg & 8)) ? p.aux[pi] : 0.f;
       if (lane == 0) mbar_wait_sleep(&tfull[buf], (tph >> buf) & 1u);
@@ -196,14 +214,15 @@ __device__ __forceinline__ void epilogue_role(const BParams &p, uint32_t tmem,
       fence_after();
       const uint32_t taddr =
           tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * 256);
+      TmemRelease<CG> rel{&tempty[buf], lane};
       if (p.dbg & 1)  // timing experiment: no TMEM drain / math
-        release_tmem(&tempty[buf], lane);
+        rel();
       else
-        epi_tile<W8>(taddr, h, p.spt, p.w, ax, valid, acc, &tempty[buf], lane);
+        epi_tile<W8>(taddr, h, p.spt, p.w, ax, valid, acc, rel);
       buf ^= 1u;
     }
     // item end: per set, fixed xor tree over the 32 lanes, then the four
-    // lane quarters in order
+    // lane quarters in order (then the pair's two CTAs in order)
 #pragma unroll
     for (int u = 0; u < MAXS; ++u) {
       const int s = h + 2 * u;
@@ -215,17 +234,55 @@ __device__ __forceinline__ void epilogue_role(const BParams &p, uint32_t tmem,
       }
     }
     asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
-    if (ew == 0 && lane < p.spt) {
+    if (ew == 0) {
+      const bool mine = lane < p.spt;
+      const double tot =
+          mine ? ((red[lane] + red[kMaxSpt + lane]) + red[2 * kMaxSpt + lane]) +
+                     red[3 * kMaxSpt + lane]
+               : 0.0;
       const int64_t j = st * p.spt + lane;
-      if (j < p.l)
-        p.partial[sp * p.l + j] =
-            ((red[lane] + red[kMaxSpt + lane]) + red[2 * kMaxSpt + lane]) +
-            red[3 * kMaxSpt + lane];
+      if constexpr (CG == 1) {
+        if (mine && j < p.l) p.partial[sp * p.l + j] = tot;
+      } else if (rank == 1) {
+        if (lane == 0) mbar_wait_cluster(xempty, xph ^ 1u);
+        __syncwarp();
+        if (mine) {
+          asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(
+                           mapa(&xbuf[lane], 0)),
+                       "d"(tot)
+                       : "memory");
+          asm volatile("fence.acq_rel.cluster;" ::: "memory");
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(mapa(xfull, 0));
+      } else {
+        if (lane == 0) mbar_wait_cluster(xfull, xph);
+        __syncwarp();
+        if (mine && j < p.l) p.partial[sp * p.l + j] = tot + xbuf[lane];
+        asm volatile("fence.acq_rel.cluster;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(mapa(xempty, 1));
+      }
+      xph ^= 1u;
     }
     asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
   }
 }
 
+template <int CG>
+__device__ __forceinline__ void issue_mma(const BParams &p, uint32_t d,
+                                          uint64_t ad, uint64_t bd, int kc,
+                                          int j) {
+  if (p.dbg & 2) return;  // timing experiment: no MMA
+  if constexpr (CG == 2)
+    umma_f16_pair(d, ad + (uint64_t)(2 * j), bd + (uint64_t)(2 * j), p.idesc,
+                  (kc | j) ? 1u : 0u);
+  else
+    umma_f16(d, ad + (uint64_t)(2 * j), bd + (uint64_t)(2 * j), p.idesc,
+             (kc | j) ? 1u : 0u);
+}
+
+template <int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     batch_tc_kernel(const __grid_constant__ CUtensorMap map_p,
                     const __grid_constant__ CUtensorMap map_s,
@@ -233,7 +290,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char *smem = (unsigned char *)(((uintptr_t)smem_raw + 1023) &
                                           ~(uintptr_t)1023);
-  const int b_chunk = p.ncols * 128;  // bytes of one set-tile K-chunk
+  const int bh = p.ncols / CG;        // set-tile rows held by this CTA
+  const int b_chunk = bh * 128;       // bytes of one set-tile K-chunk half
   const int sb_bytes = p.bstream ? 0 : p.kchunks * b_chunk;
   const int stage_bytes = A_CHUNK + (p.bstream ? b_chunk : 0);
   unsigned char *sb = smem;                        // stationary set tile
@@ -245,10 +303,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t *tempty = tfull + 2;                    // [2]
   uint64_t *bfull = tempty + 2;                    // [1]
   uint64_t *bempty = bfull + 1;                    // [1]
-  uint32_t *tmem_slot = (uint32_t *)(bempty + 1);
+  uint64_t *xfull = bempty + 1;                    // [1] pair exchange (CTA 0)
+  uint64_t *xempty = xfull + 1;                    // [1] pair exchange (CTA 1)
+  uint32_t *tmem_slot = (uint32_t *)(xempty + 1);
   double *red = (double *)(tmem_slot + 4);         // [4][kMaxSpt]
+  double *xbuf = red + 4 * kMaxSpt;                // [kMaxSpt]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = CG == 2 ? cluster_rank() : 0u;
+  const int64_t pair = blockIdx.x / CG, npairs = gridDim.x / CG;
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < p.stages; ++s) {
       mbar_init(&full[s], 1);
@@ -256,55 +319,81 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], kEpiWarps);
+      mbar_init(&tempty[b], kEpiWarps * CG);
     }
     mbar_init(bfull, 1);
     mbar_init(bempty, 1);
+    mbar_init(xfull, 1);
+    mbar_init(xempty, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&map_p));
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&map_s));
   }
   if (warp == 1) {
-    asm volatile(
-        "tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::
-            "r"(su32(tmem_slot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (CG == 2) {
+      asm volatile(
+          "tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::
+              "r"(su32(tmem_slot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile(
+          "tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::
+              "r"(su32(tmem_slot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   fence_before();
   __syncthreads();
+  if constexpr (CG == 2) cluster_sync();
   fence_after();
   const uint32_t tmem = *tmem_slot;
   const int64_t items = p.set_tiles * p.splits;
 
   if (warp == 0) {
     // -------------------------------------------------------------- producer
+    // Each CTA loads its own point rows and its half of the set tile; the
+    // completions are counted on the leader's barriers (CG = 2).
     if (lane == 0) {
       int stage = 0;
       uint32_t ph = 0, bph = 0;
-      for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+      const uint32_t bfull_c = CG == 2 ? mapa(bfull, 0) : 0u;
+      for (int64_t it = pair; it < items; it += npairs) {
         const int64_t st = it % p.set_tiles, sp = it / p.set_tiles;
-        const int srow = (int)(st * p.ncols);
+        const int srow = (int)(st * p.ncols) + (int)rank * bh;
         if (!p.bstream) {
           mbar_wait_sleep(bempty, bph ^ 1);
           bph ^= 1;
-          mbar_expect_tx(bfull, (uint32_t)sb_bytes);
-          for (int kc = 0; kc < p.kchunks; ++kc)
-            tma_load_2d(sb + kc * b_chunk, &map_s, bfull, kc * KCH, srow);
+          if (rank == 0) mbar_expect_tx(bfull, (uint32_t)(CG * sb_bytes));
+          for (int kc = 0; kc < p.kchunks; ++kc) {
+            if constexpr (CG == 2)
+              tma_load_2d_pair(sb + kc * b_chunk, &map_s, bfull_c, kc * KCH, srow);
+            else
+              tma_load_2d(sb + kc * b_chunk, &map_s, bfull, kc * KCH, srow);
+          }
         }
         const int64_t p0 = sp * p.split_pts;
         const int64_t p1 = min(p.n, p0 + p.split_pts);
-        for (int64_t pt = p0; pt < p1; pt += BM) {
+        for (int64_t pt = p0; pt < p1; pt += BM * CG) {
+          const int prow = (int)(pt + BM * rank);
           for (int kc = 0; kc < p.kchunks; ++kc) {
             mbar_wait_sleep(&empty[stage], ph ^ 1);
             unsigned char *dst = sa + stage * stage_bytes;
             if (p.dbg & 4) {  // timing experiment: no point-operand traffic
-              mbar_arrive(&full[stage]);
+              if (rank == 0) mbar_arrive(&full[stage]);
             } else {
-              mbar_expect_tx(&full[stage], (uint32_t)stage_bytes);
-              tma_load_2d(dst, &map_p, &full[stage], kc * KCH, (int)pt);
-              if (p.bstream)
-                tma_load_2d(dst + A_CHUNK, &map_s, &full[stage], kc * KCH,
-                            srow);
+              if (rank == 0)
+                mbar_expect_tx(&full[stage], (uint32_t)(CG * stage_bytes));
+              if constexpr (CG == 2) {
+                const uint32_t fc = mapa(&full[stage], 0);
+                tma_load_2d_pair(dst, &map_p, fc, kc * KCH, prow);
+                if (p.bstream)
+                  tma_load_2d_pair(dst + A_CHUNK, &map_s, fc, kc * KCH, srow);
+              } else {
+                tma_load_2d(dst, &map_p, &full[stage], kc * KCH, prow);
+                if (p.bstream)
+                  tma_load_2d(dst + A_CHUNK, &map_s, &full[stage], kc * KCH,
+                              srow);
+              }
             }
             if (++stage == p.stages) {
               stage = 0;
@@ -316,18 +405,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    // (the leader CTA's single thread issues for the pair)
+    if (lane == 0 && rank == 0) {
       const uint64_t a_base = sw128_desc(su32(sa));
       const uint64_t b_base = sw128_desc(su32(sb));
       const uint32_t a_step = (uint32_t)(stage_bytes >> 4);
       const uint32_t b_step = (uint32_t)(b_chunk >> 4);
       int stage = 0;
       uint32_t ph = 0, bph = 0, tph = 0, buf = 0;
-      for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+      for (int64_t it = pair; it < items; it += npairs) {
         const int64_t sp = it / p.set_tiles;
         const int64_t p0 = sp * p.split_pts;
         const int64_t p1 = min(p.n, p0 + p.split_pts);
-        const int ntiles = (int)((p1 - p0 + BM - 1) / BM);
+        const int ntiles = (int)((p1 - p0 + BM * CG - 1) / (BM * CG));
         const int nev = ntiles * p.kchunks;
         if (!p.bstream) {
           mbar_wait(bfull, bph);
@@ -351,10 +441,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           // queued MMAs.  (Splitting them -- B stage before MMA nk-2, buffer
           // before nk-1, the better placement for K3 -- measured 1.5x
           // slower here: profiles/r01_k4_probe.log.)
-          const int wf = nk > 2 ? nk - 2 : 0;
-          const int wt = wf;
+          const int head = nk > 2 ? nk - 2 : 0;
           const bool last = (kc == p.kchunks - 1);
-          const bool more = e + 1 < nev;
           int nstage = stage + 1;
           uint32_t nph = ph;
           if (nstage == p.stages) {
@@ -362,24 +450,25 @@ __global__ void __launch_bounds__(kThreads, 1)
             nph ^= 1u;
           }
 #pragma unroll 1
-          for (int j = 0; j < nk; ++j) {
-            if (more && last && j == wt) {
+          for (int j = 0; j < head; ++j)
+            issue_mma<CG>(p, d, ad, bd, kc, j);
+          if (e + 1 < nev) {
+            if (last) {
               const uint32_t nb = buf ^ 1u;
               mbar_wait(&tempty[nb], ((tph >> nb) & 1u) ^ 1u);
               tph ^= 1u << nb;
-              fence_after();
             }
-            if (more && j == wf) {
-              mbar_wait(&full[nstage], nph);
-              fence_after();
-            }
-            if (!(p.dbg & 2))
-              umma_f16(d, ad + (uint64_t)(2 * j), bd + (uint64_t)(2 * j),
-                       p.idesc, (kc | j) ? 1u : 0u);
+            mbar_wait(&full[nstage], nph);
+            fence_after();
           }
-          umma_commit(&empty[stage]);
+#pragma unroll 1
+          for (int j = head; j < nk; ++j)
+            issue_mma<CG>(p, d, ad, bd, kc, j);
+          if constexpr (CG == 2) umma_commit_pair(&empty[stage]);
+          else umma_commit(&empty[stage]);
           if (last) {
-            umma_commit(&tfull[buf]);
+            if constexpr (CG == 2) umma_commit_pair(&tfull[buf]);
+            else umma_commit(&tfull[buf]);
             buf ^= 1u;
             kc = 0;
           } else {
@@ -388,15 +477,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           stage = nstage;
           ph = nph;
         }
-        if (!p.bstream) umma_commit(bempty);
+        if (!p.bstream) {
+          if constexpr (CG == 2) umma_commit_pair(bempty);
+          else umma_commit(bempty);
+        }
       }
     }
     __syncwarp();
   } else {
     // -------------------------------------------------------------- epilogue
     switch (p.w >> 3) {
-#define EXEM_EPI_CASE(W) \
-  case W: epilogue_role<W>(p, tmem, tfull, tempty, red, warp, lane, items); break;
+#define EXEM_EPI_CASE(W)                                                     \
+  case W:                                                                    \
+    epilogue_role<CG, W>(p, tmem, tfull, tempty, red, xbuf, xfull, xempty,   \
+                         warp, lane, items, rank, pair, npairs);             \
+    break;
       EXEM_EPI_CASE(1) EXEM_EPI_CASE(2) EXEM_EPI_CASE(3) EXEM_EPI_CASE(4)
       EXEM_EPI_CASE(5) EXEM_EPI_CASE(6) EXEM_EPI_CASE(7) EXEM_EPI_CASE(8)
       EXEM_EPI_CASE(9) EXEM_EPI_CASE(10) EXEM_EPI_CASE(11) EXEM_EPI_CASE(12)
@@ -412,10 +507,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   fence_before();
   __syncthreads();
+  if constexpr (CG == 2) cluster_sync();
   if (warp == 1) {
     fence_after();
-    asm volatile(
-        "tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    if constexpr (CG == 2)
+      asm volatile(
+          "tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    else
+      asm volatile(
+          "tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
 }
 
@@ -550,21 +650,29 @@ int exem_batch_eval_tc(int dtype, const void *xp, int64_t n, const void *aux,
   prm.ncols = nc;
   prm.ksteps = (int)ceil_div(d + kTcConst, 16);
   prm.kchunks = (int)(kp / KCH);
-  prm.idesc = make_idesc(dtype == EXEM_BF16, BM, nc);
+  // Single-CTA tiles by default.  EXEM_TCB_CG=2 selects CTA pairs
+  // (cta_group::2, M = 256, each CTA holding half of the set tile, 9 instead
+  // of 5 point-chunk stages at d = 256): correct (tests) but measured no
+  // faster at d = 256 and 1.4x slower at d = 100 (tools/k4_cg_compare.sh,
+  // profiles/r01_k4_probe.log) -- the per-chunk cross-SM handshake costs
+  // more than the deeper ring saves.
+  int cg = 1;
+  if (const char *e = getenv("EXEM_TCB_CG")) cg = atoi(e) == 2 ? 2 : 1;
+  prm.idesc = make_idesc(dtype == EXEM_BF16, BM * cg, nc);
   prm.aux = (const float *)aux;
   {
     const char *dbg = getenv("EXEM_TCB_DEBUG");
     prm.dbg = dbg ? atoi(dbg) : 0;
   }
   prm.partial = partial;
-  const int b_chunk = nc * 128;
+  const int b_chunk = (nc / cg) * 128;
   const int avail = kSmemBudget - kBarBytes - 1024;
   // set tile stationary when it leaves room for >= 3 point-chunk stages
   const bool bstream = (avail - prm.kchunks * b_chunk) / A_CHUNK < 3;
   const int sb_bytes = bstream ? 0 : prm.kchunks * b_chunk;
   const int stage_bytes = A_CHUNK + (bstream ? b_chunk : 0);
   int stages = (avail - sb_bytes) / stage_bytes;
-  if (stages > 8) stages = 8;
+  if (stages > 16) stages = 16;
   if (stages < 2) return fail(EXEM_ERR_UNSUPPORTED, "set tile too large for smem");
   prm.stages = stages;
   prm.bstream = bstream ? 1 : 0;
@@ -572,15 +680,53 @@ int exem_batch_eval_tc(int dtype, const void *xp, int64_t n, const void *aux,
                       kBarBytes + 1024;
   CUtensorMap mp, ms;
   if (int rc = make_map(&mp, xp, dtype, exem_tc_rows(n), kp, BM)) return rc;
-  if (int rc = make_map(&ms, xs, dtype, exem_tc_set_rows(l, k_max), kp, nc))
+  if (int rc = make_map(&ms, xs, dtype, exem_tc_set_rows(l, k_max), kp,
+                        nc / cg))
     return rc;
   const int64_t items = prm.set_tiles * splits;
-  const unsigned grid = (unsigned)(items < sms ? items : sms);
-  cudaError_t e = cudaFuncSetAttribute(
-      batch_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = (cudaStream_t)stream;
+  cudaError_t e;
+  if (cg == 2) {
+    e = cudaFuncSetAttribute(batch_tc_kernel<2>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+    if (e != cudaSuccess)
+      return fail(EXEM_ERR_CUDA, "smem attr: %s", cudaGetErrorString(e));
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int clusters = 0;
+    cfg.gridDim = dim3((unsigned)(sms & ~1));
+    e = cudaOccupancyMaxActiveClusters(&clusters, batch_tc_kernel<2>, &cfg);
+    if (e != cudaSuccess || clusters < 1)
+      return fail(EXEM_ERR_CUDA, "no co-resident CTA pairs: %s",
+                  cudaGetErrorString(e));
+    const int64_t pairs = items < clusters ? items : clusters;
+    cfg.gridDim = dim3((unsigned)(2 * pairs));
+    if (getenv("EXEM_TCB_VERBOSE"))
+      fprintf(stderr, "batch_tc<2>: clusters=%d grid=%u stages=%d smem=%zu "
+              "bstream=%d\n", clusters, cfg.gridDim.x, stages, smem,
+              (int)bstream);
+    e = cudaLaunchKernelEx(&cfg, batch_tc_kernel<2>, mp, ms, prm);
+  } else {
+    e = cudaFuncSetAttribute(batch_tc_kernel<1>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+    if (e != cudaSuccess)
+      return fail(EXEM_ERR_CUDA, "smem attr: %s", cudaGetErrorString(e));
+    cfg.gridDim = dim3((unsigned)(items < sms ? items : sms));
+    e = cudaLaunchKernelEx(&cfg, batch_tc_kernel<1>, mp, ms, prm);
+  }
   if (e != cudaSuccess)
-    return fail(EXEM_ERR_CUDA, "smem attr: %s", cudaGetErrorString(e));
-  batch_tc_kernel<<<grid, kThreads, smem, (cudaStream_t)stream>>>(mp, ms, prm);
+    return fail(EXEM_ERR_CUDA, "batch_tc_kernel launch: %s",
+                cudaGetErrorString(e));
   EXEM_LAUNCH_CHECK("batch_tc_kernel");
   return EXEM_OK;
 }

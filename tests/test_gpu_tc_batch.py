@@ -109,3 +109,16 @@ def test_tc_batch_large_sets_use_simt_path():
     assert not E.tc_batch_supported(BF16, batch.k_max)
     vals = pb.evaluate_batch(Evaluator(), g, batch)
     _check(g, sets, vals)
+
+
+def test_tc_batch_cta_pair_variant(monkeypatch):
+    """The cta_group::2 variant of K4-TC (EXEM_TCB_CG=2: M = 256 over a CTA
+    pair, set tile split across the pair, per-set sums combined through
+    DSMEM) against the fp64 oracle and the single-CTA kernel."""
+    g, sets = _case(BF16, 9000, 100, 50, 1, 50, seed=17)
+    batch = EvaluationBatch.from_sets([g.matrix[i] for i in sets])
+    one = pb.evaluate_batch(Evaluator(), g, batch)
+    monkeypatch.setenv("EXEM_TCB_CG", "2")
+    two = pb.evaluate_batch(Evaluator(), g, batch)
+    _check(g, sets, two, nref=20)
+    np.testing.assert_allclose(two, one, rtol=1e-6, atol=1e-6)
