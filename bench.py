@@ -48,8 +48,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=47)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
-    ap.add_argument("--n", type=int, default=1_000_000)
-    ap.add_argument("--d", type=int, default=100)
+    ap.add_argument("--points", dest="n", type=int, default=1_000_000)
+    ap.add_argument("--dim", dest="d", type=int, default=100)
     ap.add_argument("--precision", default="bf16", choices=PRECISION_CHOICES)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
@@ -210,10 +210,19 @@ def main():
                                                    build_sharded_ground)
     from paper_2101_08763_b200.optimize import GreedyRun
 
+    # EXEM_BENCH_SHARE_GPU=1 (testing only): every rank on cuda:0 over gloo,
+    # to exercise the N > 1 code path on a one-GPU box
+    share = os.environ.get("EXEM_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl",
+                                    device_id=torch.device("cuda", local))
     prec = pb.Precision.from_name(args.precision)
     n, d = args.n, args.d
     k = args.warmup + args.steps
@@ -307,7 +316,11 @@ def main():
     tfile = ROOT / "profiles" / "gains_tc_traffic.json"
     if half and tfile.exists():
         try:
-            traffic = json.loads(tfile.read_text()).get("bytes_per_launch")
+            tj = json.loads(tfile.read_text())
+            # the ncu capture is of one C4 launch on one GPU: only valid for
+            # that configuration
+            if (tj.get("n"), tj.get("d"), tj.get("world")) == (n, d, world):
+                traffic = tj.get("bytes_per_launch")
         except Exception:
             traffic = None
 
@@ -375,10 +388,40 @@ def main():
                          "api": "build_ground_set(numpy) + greedy_maximize(k)",
                          "picks_match_device_run":
                          list(res.exemplar_indices) == [int(x) for x in picks]}
+    elif world > 1 and not args.no_e2e:
+        # e2e through the public multi-GPU API: every rank uploads V from host
+        # memory (build_sharded_ground: candidate replica + its row shard) and
+        # runs the row-sharded Greedy (NCCL all-reduce per step); the result
+        # picks/values come back to the host.  Device time = max over ranks.
+        from paper_2101_08763_b200.distributed import sharded_greedy
+
+        del run, ops, sg
+        torch.cuda.empty_cache()
+        torch.cuda.synchronize()
+        dist.barrier()
+        t_start = time.perf_counter()
+        sg2 = build_sharded_ground(V, prec, rank, world, device=local)
+        picks2, _ = sharded_greedy(sg2, k)
+        torch.cuda.synchronize()
+        t_e2e = torch.tensor([time.perf_counter() - t_start],
+                             dtype=torch.float64, device="cuda")
+        dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
+        if rank == 0:
+            e2e_evals = float(sum(n - t for t in range(k)))
+            h2d = world * (n * d * prec.bytes_per_value +
+                           d * prec.bytes_per_value)
+            d2h = world * (2 * 8 * k + 8)
+            result["e2e"] = {"value": e2e_evals / float(t_e2e.item()),
+                             "unit": UNIT, "h2d_bytes_per_step": h2d / k,
+                             "d2h_bytes_per_step": d2h / k,
+                             "seconds": float(t_e2e.item()), "steps": k,
+                             "api": "build_sharded_ground(numpy) + "
+                                    "sharded_greedy(k) on every rank",
+                             "picks_match_device_run":
+                             list(picks2) == [int(x) for x in picks]}
     elif rank == 0:
         result["e2e"] = {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0,
-                         "d2h_bytes_per_step": 0,
-                         "note": "multi-GPU e2e not measured in this round"}
+                         "d2h_bytes_per_step": 0, "note": "--no-e2e"}
     if rank == 0:
         print(json.dumps(result), flush=True)
     if world > 1:

@@ -96,8 +96,9 @@ int exem_ground_prepare(int dtype, const void *src, int64_t n, int64_t d,
  *            partials (the final step of K1/K2 sums; with per-slice block
  *            partials at their global offsets the result is bit-identical
  *            to the resident computation).
- * K1 with aux_sum == NULL and K2 with sum_out == NULL leave their
- * per-256-point block partials in `scratch` instead of reducing them.
+ * K1 with aux_sum == NULL, K2 (set_min) with sum_out == NULL and
+ * greedy_update with msum == NULL leave their per-256-point block partials
+ * in `scratch` instead of reducing them.
  */
 int exem_host_register(void *host, int64_t bytes);
 int exem_host_unregister(void *host);

@@ -834,6 +834,9 @@ int exem_greedy_update(int dtype, const void *vt, int64_t ld, int64_t n,
         sel_idx, step, (C *)m, (S *)xp, kp, scratch);
     EXEM_LAUNCH_CHECK("greedy_update_kernel");
   });
+  // msum == NULL: leave the per-256-point block partials of sum_i m_i in
+  // scratch (a streamed slice writes them at its global block offset)
+  if (!msum) return EXEM_OK;
   return reduce_fixed(scratch, blocks, msum, step, st);
 }
 

@@ -198,6 +198,18 @@ def greedy_maximize(ground: GroundSet, k: int,
     if k <= 0:
         return OptimizationResult(exemplar_indices=(), values=(), evaluations=0)
     _effective_precision(evaluator, ground)
+    if ground.streamed:
+        # V over the device budget: candidates and points stream through in
+        # resident chunks / split-aligned slices (streaming.py); bit-identical
+        # to the resident run
+        from .streaming import stream_greedy
+
+        idx, msum = stream_greedy(ground, k, evaluator.device)
+        return OptimizationResult(
+            exemplar_indices=tuple(int(i) for i in idx[:k]),
+            values=trajectory_values(ground, msum[:k]),
+            evaluations=sum(ground.n - i for i in range(k)),
+        )
     dg = ground.on_device(evaluator.device)
     from .device import torch
 

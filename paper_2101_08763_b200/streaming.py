@@ -360,6 +360,156 @@ def stream_packed_sums(ground, values, d, k_max, l, cardinalities,
         gs.close()
 
 
+# ------------------------------------------------------------ streamed Greedy
+def stream_greedy(ground, k: int, device=None):
+    """Greedy (optimize.py:33-82) over a streamed ground set.
+
+    The optimizer-aware state stays on the device (m_i for all n points, the
+    selection mask, the gains); V streams through.  Candidates are V itself,
+    so they are processed in resident chunks of ``cand_rows`` rows: per step
+    and candidate chunk, every point slice is streamed through K3 (SIMT or
+    tcgen05) into the [splits][chunk] partials, then K6 reduces them into
+    the chunk's gains.  The m-update with the previous pick (K2) is applied
+    to each slice on its first pass of the next step (and in one final
+    pass), and its per-block partial sums give msum exactly as the resident
+    run.  Everything is bit-identical to the resident Greedy.  Returns
+    (indices, msum) as host arrays.
+    """
+    from .device import compute_torch_dtype, padded_rows, to_device_bytes, torch
+
+    t = torch()
+    lib = N.lib()
+    prec = ground.precision
+    n, d = ground.n, ground.d
+    sp = int(lib.split_points(n))
+    splits = -(-n // sp)
+    cs = _csize(prec)
+    half = prec.is_half
+    budget = ground.device_budget
+    state = n * cs + n + 8 * n + 3 * 8 * k + _margin(n) + \
+        int(lib.reduce_scratch(max(n, 1))) * 8
+    free = budget - state
+    # candidate chunk: half of what is left (rows, multiple of 256), the
+    # other half for the streaming ring
+    per_cand = layout_bytes(256, d, prec, with_src=True) // 256 + splits * 8
+    cand_rows = max(256, min(-(-n // 256) * 256,
+                             (free // 2) // per_cand // 256 * 256))
+    cand_bytes = layout_bytes(cand_rows, d, prec, with_src=True) + \
+        splits * cand_rows * 8
+    gs = GroundStream(ground, free - cand_bytes, device)
+    try:
+        with t.cuda.device(gs.idx):
+            dev = gs.dev
+            st = N.stream_handle(dev)
+            cdt = compute_torch_dtype(prec)
+            m = t.empty(n, dtype=cdt, device=dev)
+            selected = t.zeros(n, dtype=t.uint8, device=dev)
+            gains = t.empty(n, dtype=t.float64, device=dev)
+            sel_idx = t.zeros(k, dtype=t.int64, device=dev)
+            sel_gain = t.zeros(k, dtype=t.float64, device=dev)
+            msum = t.zeros(k, dtype=t.float64, device=dev)
+            zero_idx = t.zeros(1, dtype=t.int64, device=dev)
+            scratch = t.empty(int(lib.reduce_scratch(max(n, 1))),
+                              dtype=t.float64, device=dev)
+            partial = t.empty((splits, cand_rows), dtype=t.float64, device=dev)
+            d_pad = int(lib.pad_dims(d))
+            # chosen exemplar in a one-column SIMT layout [d_pad][256]
+            chosen = t.zeros((d_pad, 256), dtype=cdt, device=dev)
+            cnorm = t.empty(1, dtype=t.float64, device=dev)
+            # candidate chunk layouts
+            c_src = t.empty(cand_rows * d * prec.bytes_per_value,
+                            dtype=t.uint8, device=dev)
+            c_ld = int(lib.pad_points(cand_rows))
+            c_vt = t.empty(d_pad * c_ld, dtype=cdt, device=dev)
+            c_norms = t.empty(c_ld, dtype=t.float64, device=dev)
+            c_aux = t.empty(c_ld, dtype=cdt, device=dev)
+            c_xc = None
+            if half:
+                tdt = t.bfloat16 if prec.tag == N.BF16 else t.float16
+                c_xc = t.empty((int(lib.tc_rows(cand_rows)),
+                                int(lib.tc_kp(d))), dtype=tdt, device=dev)
+            host_ptr = gs._host_ptr
+
+            def load_candidates(c0, c1):
+                rows = c1 - c0
+                lib.h2d_rows(N.ptr(c_src), host_ptr, n, c0, rows, d,
+                             prec.bytes_per_value, st)
+                lib.ground_prepare(prec.tag, N.ptr(c_src), rows, d,
+                                   N.ptr(gs.e0), N.ptr(c_vt),
+                                   int(lib.pad_points(rows)), N.ptr(c_norms),
+                                   N.ptr(c_aux), None, N.ptr(scratch), st)
+                if half:
+                    lib.tc_pack_candidates(prec.tag, N.ptr(c_vt),
+                                           int(lib.pad_points(rows)), rows, d,
+                                           N.ptr(c_norms), N.ptr(c_xc), st)
+
+            def update_slice(slot, r0, r1, step_prev):
+                """m <- min(m, d(v, chosen)) on this slice; block partials of
+                sum m at the slice's global offset."""
+                lib.greedy_update(prec.tag, N.ptr(slot.vt), slot.ld, r1 - r0,
+                                  d, N.ptr(slot.norms), N.ptr(chosen), 256,
+                                  N.ptr(cnorm), N.ptr(zero_idx), 0,
+                                  N.c_void_p(m.data_ptr() + r0 * cs), None,
+                                  0, None, gs.block_ptr(r0), st)
+
+            def finish_msum(step):
+                lib.sum_fixed(N.ptr(gs.block_partials), -(-n // 256),
+                              N.ptr(msum), step, st)
+
+            # S = {}: m = aux (the resident greedy_init), streamed
+            for slot, r0, r1 in gs.slices(pack_points=False):
+                t_ptr = N.c_void_p(m.data_ptr() + r0 * cs)
+                lib.greedy_init(prec.tag, N.ptr(slot.aux), r1 - r0, t_ptr,
+                                N.ptr(cnorm), N.ptr(scratch), st)
+            for step in range(k):
+                for c0 in range(0, n, cand_rows):
+                    c1 = min(n, c0 + cand_rows)
+                    cl = c1 - c0
+                    load_candidates(c0, c1)
+                    for slot, r0, r1 in gs.slices(pack_points=False):
+                        rows = r1 - r0
+                        if step > 0 and c0 == 0:
+                            update_slice(slot, r0, r1, step - 1)
+                        s0, ns = r0 // sp, -(-rows // sp)
+                        part = N.c_void_p(partial.data_ptr() + s0 * cl * 8)
+                        m_ptr = N.c_void_p(m.data_ptr() + r0 * cs)
+                        if half:
+                            lib.tc_pack_points(prec.tag, N.ptr(slot.vt),
+                                               slot.ld, rows, d,
+                                               N.ptr(slot.norms), m_ptr,
+                                               N.ptr(slot.xp0()), st)
+                            lib.greedy_gains_tc(prec.tag, N.ptr(c_xc), cl,
+                                                N.ptr(slot.xp0()), rows, d, sp,
+                                                part, ns, st)
+                        else:
+                            lib.greedy_gains_simt(prec.tag, N.ptr(c_vt),
+                                                  int(lib.pad_points(cl)),
+                                                  N.ptr(c_norms), cl,
+                                                  N.ptr(slot.vt), slot.ld,
+                                                  N.ptr(slot.norms), m_ptr,
+                                                  rows, d, sp, part, ns, st)
+                    if step > 0 and c0 == 0:
+                        finish_msum(step - 1)
+                    lib.reduce_partials(N.ptr(partial), splits, cl, 2.0,
+                                        N.c_void_p(gains.data_ptr() + c0 * 8),
+                                        st)
+                lib.argmax_select(N.ptr(gains), n, N.ptr(selected), None, step,
+                                  N.ptr(sel_idx), N.ptr(sel_gain),
+                                  N.ptr(scratch), st)
+                c = int(sel_idx[step].item())
+                row = padded_rows(ground.matrix[c:c + 1], d_pad, prec, dev)
+                chosen[:, 0].copy_(row[0])
+                lib.row_norms(prec.tag, N.ptr(row), 1, d, d_pad, N.ptr(cnorm),
+                              st)
+            # the last pick's m-update (msum[k-1])
+            for slot, r0, r1 in gs.slices(pack_points=False):
+                update_slice(slot, r0, r1, k - 1)
+            finish_msum(k - 1)
+            return sel_idx.cpu().numpy(), msum.cpu().numpy()
+    finally:
+        gs.close()
+
+
 def _margin(n: int) -> int:
     """Device bytes a streamed pass needs besides the ring and the batch:
     the global block-partial array, e0 and small scalars."""
@@ -372,4 +522,5 @@ def fits_resident(n: int, d: int, precision, budget) -> bool:
 
 __all__ = ["StreamPlan", "plan_slices", "resident_bytes", "layout_bytes",
            "GroundStream", "stream_build", "stream_set_min",
-           "stream_packed_sums", "batch_device_bytes", "fits_resident"]
+           "stream_packed_sums", "batch_device_bytes", "fits_resident",
+           "stream_greedy"]

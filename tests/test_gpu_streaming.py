@@ -105,3 +105,24 @@ def test_streamed_budget_errors():
     assert g.streamed
     with pytest.raises(pb.OutOfMemoryError):
         g.on_device()
+
+
+@pytest.mark.parametrize("prec", [BF16, P32, P64])
+def test_streamed_greedy_matches_resident(prec):
+    """Greedy over a streamed ground set (candidate chunks x point slices,
+    m kept on device) picks the same exemplars with bit-identical values."""
+    rng = np.random.default_rng(8)
+    n, d, k = 12_000, 24, 4
+    data = rng.standard_normal((n, d))
+    gr = pb.build_ground_set(data, precision=prec)
+    ref = pb.greedy_maximize(gr, k=k)
+    lib = N.lib()
+    sp = int(lib.split_points(n))
+    budget = int(0.9 * S.resident_bytes(n, d, prec))
+    gs = pb.build_ground_set(data, precision=prec, device_budget=budget)
+    assert gs.streamed
+    res = pb.greedy_maximize(gs, k=k)
+    assert res.exemplar_indices == ref.exemplar_indices
+    assert res.values == ref.values
+    assert res.evaluations == ref.evaluations
+    assert sp > 0
