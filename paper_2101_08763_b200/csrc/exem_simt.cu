@@ -741,10 +741,14 @@ int exem_sum_fixed(const double *in, int64_t count, double *out,
 
 int exem_host_register(void *host, int64_t bytes) {
   cudaError_t e = cudaHostRegister(host, (size_t)bytes, cudaHostRegisterDefault);
-  if (e == cudaErrorHostMemoryAlreadyRegistered) {
+  if (e != cudaSuccess && e != cudaErrorHostMemoryAlreadyRegistered) {
+    // a read-only mapping (e.g. a memory-mapped .exem payload) can only be
+    // locked read-only
     cudaGetLastError();
-    return EXEM_OK;
+    e = cudaHostRegister(host, (size_t)bytes, cudaHostRegisterReadOnly);
   }
+  cudaGetLastError();  // never leave a sticky error for the next launch check
+  if (e == cudaErrorHostMemoryAlreadyRegistered) return EXEM_OK;
   if (e != cudaSuccess)
     return fail(EXEM_ERR_CUDA, "cudaHostRegister: %s", cudaGetErrorString(e));
   return EXEM_OK;

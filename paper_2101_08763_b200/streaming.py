@@ -115,8 +115,13 @@ def pin_host(ground) -> None:
     if pinned is None or pinned.get("done"):
         return
     m = ground.matrix
-    N.lib().host_register(c_void_p(m.ctypes.data), m.nbytes)
     pinned["done"] = True
+    try:
+        N.lib().host_register(c_void_p(m.ctypes.data), m.nbytes)
+    except Exception:
+        # e.g. a read-only file mapping the driver refuses to lock: the 2-D
+        # DMA then stages through pageable memory (slower, still correct)
+        return
     weakref.finalize(ground, _unpin, m, m.ctypes.data)
 
 

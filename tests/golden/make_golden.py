@@ -151,6 +151,14 @@ def main(argv):
                     if key.startswith("c1_"):
                         g[key] = z[key]
 
+    # ---- the reference's benchmark problem generator (src/bench.py:66-93)
+    from exembatch.bench import generate_problem
+
+    for tag, prec in (("32", P32), ("64", P64), ("16", P16)):
+        ground, batch = generate_problem(50, 4, 3, 5, 11, prec)
+        g[f"gen{tag}_values"] = np.asarray(ground.matrix)
+        g[f"gen{tag}_sets"] = np.stack([np.asarray(s) for s in batch.sets])
+
     np.savez_compressed(OUT / "golden.npz", **g)
     (OUT / "hand.json").write_text(json.dumps(hand, indent=1) + "\n")
     print(f"wrote {len(g)} arrays, {len(hand)} hand cases")
