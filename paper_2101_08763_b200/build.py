@@ -54,7 +54,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     objs = []
     for src in SOURCES:
         obj = build_dir / (src.stem + ".o")
-        cmd = [nvcc, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
+        extra = os.environ.get("EXEM_NVCC_FLAGS", "").split()  # experiments
+        cmd = [nvcc, *NVCC_FLAGS, *extra, "-c", str(src), "-o", str(obj)]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.run(cmd, check=True)

@@ -44,9 +44,24 @@ constexpr int BM = 128;                 // points per tile (TMEM lanes)
 constexpr int A_CHUNK = BM * 128;       // bytes of one point K-chunk
 constexpr int kThreads = 320;
 constexpr int kEpiWarps = 8;
-constexpr int kMaxSpt = 32;             // sets per set tile (w >= 8)
+constexpr int kMaxSpt = 16;             // sets per set tile (register budget of the epilogue)
 constexpr int kSmemBudget = 227 * 1024;
 constexpr int kBarBytes = 2048;
+constexpr int kTrace = 256;  // tiles traced on CTA 0
+// CTA-0 timeline for timing experiments (tools/tcb_trace.py): compiled in
+// only with -DEXEM_TCB_TRACE_BUILD (EXEM_NVCC_FLAGS at build time) -- the
+// extra live registers would otherwise spill in the epilogue.
+#ifdef EXEM_TCB_TRACE_BUILD
+#define TRB(slot, t)                                                       \
+  do {                                                                     \
+    if (p.trace != nullptr && blockIdx.x == 0 && (t) < kTrace)             \
+      p.trace[(slot) * kTrace + (t)] = clock64();                          \
+  } while (0)
+#else
+#define TRB(slot, t) \
+  do {               \
+  } while (0)
+#endif
 
 struct BParams {
   int64_t n;           // points of this slice
@@ -61,8 +76,10 @@ struct BParams {
   int kchunks;         // 64-wide K chunks per operand row
   int stages;          // point-chunk ring depth
   int bstream;         // 1: set chunks streamed with the point chunks
+  int tstage;          // 1: a ring stage holds a whole point tile (all K)
   int dbg;             // timing experiments only (EXEM_TCB_DEBUG), 0 in use
   uint32_t idesc;
+  long long *trace;    // timing experiments only (EXEM_TCB_TRACE): CTA-0 timeline
   const float *aux;    // [n] aux distances (compute type)
   double *partial;     // [splits][l]
 };
@@ -100,14 +117,15 @@ struct TmemRelease {
 //   t = min(aux_i, max(0, -2 max_e D)),  acc[u] += t   (fp64, per thread)
 template <int W8>
 struct EpiShape {
-  static constexpr int MAXS = (32 / W8 + 1) / 2;  // sets per warp (max)
+  static constexpr int SPT = 32 / W8 < kMaxSpt ? 32 / W8 : kMaxSpt;
+  static constexpr int MAXS = (SPT + 1) / 2;  // sets per warp (max)
   // sets per load batch: registers of one batch (8 per group) plus the fp64
-  // accumulators within a 128-register budget (ptxas caps this kernel at
+  // accumulators within a 120-register budget (ptxas caps this kernel at
   // 168 registers per thread)
   static constexpr int sb() {
     int best = 1;
     for (int s = 1; s <= MAXS; ++s)
-      if (s * W8 * 8 + 2 * MAXS <= 128) best = s;
+      if (s * W8 * 8 + 2 * MAXS <= 120) best = s;
     return best;
   }
   static constexpr int SB = sb();
@@ -124,7 +142,7 @@ __device__ __forceinline__ void epi_tile(
     release();
     return;
   }
-  if constexpr (W8 <= 16) {
+  if constexpr (W8 * 8 + 2 * EpiShape<W8>::MAXS <= 120) {
     constexpr int SB = EpiShape<W8>::SB;
     constexpr int NB = EpiShape<W8>::NB;
     const int nbat = (nsets + SB - 1) / SB;
@@ -155,21 +173,24 @@ __device__ __forceinline__ void epi_tile(
       }
     }
   } else {
-    // w > 128: one set per tile (spt == 1, only h == 0 has it); drain it in
-    // sub-batches of 16 groups with a running max
-    constexpr int NS = (W8 + 15) / 16;
+    // w >= 120: at most one set per warp (set h); drain it in sub-batches of
+    // 12 groups (96 registers) with a running max
+    static_assert(EpiShape<W8>::MAXS == 1, "wide sets: one set per warp");
+    constexpr int G = 12;
+    constexpr int NS = (W8 + G - 1) / G;
+    const uint32_t c0 = taddr + (uint32_t)(h * w);
     float mx = ninf;
 #pragma unroll
     for (int sb = 0; sb < NS; ++sb) {
-      uint32_t r[16][8];
+      uint32_t r[G][8];
 #pragma unroll
-      for (int g = 0; g < 16; ++g)
-        if (sb * 16 + g < W8) TMEM_LD8(taddr + 8 * (sb * 16 + g), r[g]);
+      for (int g = 0; g < G; ++g)
+        if (sb * G + g < W8) TMEM_LD8(c0 + 8 * (sb * G + g), r[g]);
       tmem_wait_ld();
       if (sb == NS - 1) release();
 #pragma unroll
-      for (int g = 0; g < 16; ++g)
-        if (sb * 16 + g < W8) mx = max8(r[g], mx);
+      for (int g = 0; g < G; ++g)
+        if (sb * G + g < W8) mx = max8(r[g], mx);
     }
     const float t = fminf(ax, fmaxf(0.f, -2.f * mx));
     if (valid) acc[0] += (double)t;
@@ -197,6 +218,10 @@ __device__ __forceinline__ void epilogue_role(const BParams &p, uint32_t tmem,
   const int h = ew >> 2;         // set parity handled by this warp
   const int row = q * 32 + lane; // point row within this CTA's tile half
   uint32_t buf = 0, tph = 0, xph = 0;
+#ifdef EXEM_TCB_TRACE_BUILD
+  int etile = 0;
+  const bool tr = warp == 2 && lane == 0;
+#endif
   for (int64_t it = pair; it < items; it += npairs) {
     const int64_t st = it % p.set_tiles, sp = it / p.set_tiles;
     const int64_t p0 = sp * p.split_pts;
@@ -208,8 +233,13 @@ __device__ __forceinline__ void epilogue_role(const BParams &p, uint32_t tmem,
       const int64_t pi = pt + BM * rank + row;
       const bool valid = pi < p1;
       const float ax = (valid && !(p.dbg & 8)) ? p.aux[pi] : 0.f;
-      if (lane == 0) mbar_wait_sleep(&tfull[buf], (tph >> buf) & 1u);
+      if (lane == 0) {
+        mbar_wait_sleep(&tfull[buf], (tph >> buf) & 1u);
+      }
       __syncwarp();
+#ifdef EXEM_TCB_TRACE_BUILD
+      if (tr) TRB(3, etile);
+#endif
       tph ^= 1u << buf;
       fence_after();
       const uint32_t taddr =
@@ -219,6 +249,10 @@ __device__ __forceinline__ void epilogue_role(const BParams &p, uint32_t tmem,
         rel();
       else
         epi_tile<W8>(taddr, h, p.spt, p.w, ax, valid, acc, rel);
+#ifdef EXEM_TCB_TRACE_BUILD
+      if (tr) TRB(4, etile);
+      ++etile;
+#endif
       buf ^= 1u;
     }
     // item end: per set, fixed xor tree over the 32 lanes, then the four
@@ -269,6 +303,60 @@ __device__ __forceinline__ void epilogue_role(const BParams &p, uint32_t tmem,
   }
 }
 
+// Issuer loop of one work item with whole-tile point stages (one barrier
+// handshake per tile, K3's scheme -- the per-chunk handshake costs ~200+
+// cycles of mbarrier latency each, profiles/r01_k4_probe.log): KS K-steps
+// unrolled at compile time, the next tile's point stage (full) acquired
+// before MMA KS-2 and its accumulator buffer (tempty) before MMA KS-1.
+template <int KS>
+__device__ __forceinline__ void k4_item_tstage(
+    const BParams &p, int ntiles, int &stage, uint32_t &ph, uint32_t &tph,
+    uint32_t &buf, int &itile, uint64_t a_base, uint32_t a_step,
+    uint64_t b_base, uint32_t b_step, uint32_t tmem, uint64_t *full,
+    uint64_t *empty, uint64_t *tfull, uint64_t *tempty) {
+  constexpr int WF = KS > 2 ? KS - 2 : 0;
+  constexpr int WT = KS > 1 ? KS - 1 : 0;
+  mbar_wait(&tempty[buf], ((tph >> buf) & 1u) ^ 1u);
+  tph ^= 1u << buf;
+  mbar_wait(&full[stage], ph);
+  fence_after();
+  for (int t = 0; t < ntiles; ++t) {
+    const uint32_t d = tmem + buf * 256u;
+    const uint64_t ad = a_base + (uint64_t)(stage * a_step);
+    const uint32_t nbuf = buf ^ 1u;
+    int nstage = stage + 1;
+    uint32_t nph = ph;
+    if (nstage == p.stages) {
+      nstage = 0;
+      nph ^= 1u;
+    }
+    const bool more = t + 1 < ntiles;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      if (ks == WF && more) {
+        mbar_wait(&full[nstage], nph);
+        fence_after();
+      }
+      if (ks == WT && more) {
+        mbar_wait(&tempty[nbuf], ((tph >> nbuf) & 1u) ^ 1u);
+        tph ^= 1u << nbuf;
+        fence_after();
+      }
+      if (!(p.dbg & 2))
+        umma_f16(d, ad + (uint64_t)((ks >> 2) * (A_CHUNK >> 4) + (ks & 3) * 2),
+                 b_base + (uint64_t)((ks >> 2) * b_step + (ks & 3) * 2),
+                 p.idesc, ks > 0 ? 1u : 0u);
+    }
+    umma_commit(&empty[stage]);
+    umma_commit(&tfull[buf]);
+    TRB(2, itile);
+    ++itile;
+    buf = nbuf;
+    stage = nstage;
+    ph = nph;
+  }
+}
+
 template <int CG>
 __device__ __forceinline__ void issue_mma(const BParams &p, uint32_t d,
                                           uint64_t ad, uint64_t bd, int kc,
@@ -293,7 +381,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int bh = p.ncols / CG;        // set-tile rows held by this CTA
   const int b_chunk = bh * 128;       // bytes of one set-tile K-chunk half
   const int sb_bytes = p.bstream ? 0 : p.kchunks * b_chunk;
-  const int stage_bytes = A_CHUNK + (p.bstream ? b_chunk : 0);
+  const int stage_bytes = p.tstage ? p.kchunks * A_CHUNK
+                                   : A_CHUNK + (p.bstream ? b_chunk : 0);
   unsigned char *sb = smem;                        // stationary set tile
   unsigned char *sa = smem + sb_bytes;             // point-chunk ring
   uint64_t *bars = (uint64_t *)(sa + p.stages * stage_bytes);
@@ -354,7 +443,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // Each CTA loads its own point rows and its half of the set tile; the
     // completions are counted on the leader's barriers (CG = 2).
     if (lane == 0) {
-      int stage = 0;
+      int stage = 0, ptile = 0;
       uint32_t ph = 0, bph = 0;
       const uint32_t bfull_c = CG == 2 ? mapa(bfull, 0) : 0u;
       for (int64_t it = pair; it < items; it += npairs) {
@@ -373,10 +462,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const int64_t p0 = sp * p.split_pts;
         const int64_t p1 = min(p.n, p0 + p.split_pts);
-        for (int64_t pt = p0; pt < p1; pt += BM * CG) {
+        for (int64_t pt = p0; pt < p1 && p.tstage; pt += BM, ++ptile) {
+          mbar_wait(&empty[stage], ph ^ 1);
+          TRB(5, ptile);
+          unsigned char *dst = sa + stage * stage_bytes;
+          if (p.dbg & 4) {
+            mbar_arrive(&full[stage]);
+          } else {
+            mbar_expect_tx(&full[stage], (uint32_t)stage_bytes);
+            for (int kc = 0; kc < p.kchunks; ++kc)
+              tma_load_2d(dst + kc * A_CHUNK, &map_p, &full[stage], kc * KCH,
+                          (int)pt);
+          }
+          TRB(6, ptile);
+          if (++stage == p.stages) {
+            stage = 0;
+            ph ^= 1;
+          }
+        }
+        for (int64_t pt = p0; pt < p1 && !p.tstage; pt += BM * CG, ++ptile) {
           const int prow = (int)(pt + BM * rank);
           for (int kc = 0; kc < p.kchunks; ++kc) {
             mbar_wait_sleep(&empty[stage], ph ^ 1);
+            if (kc == 0) TRB(5, ptile);
             unsigned char *dst = sa + stage * stage_bytes;
             if (p.dbg & 4) {  // timing experiment: no point-operand traffic
               if (rank == 0) mbar_arrive(&full[stage]);
@@ -395,6 +503,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                               srow);
               }
             }
+            if (kc == p.kchunks - 1) TRB(6, ptile);
             if (++stage == p.stages) {
               stage = 0;
               ph ^= 1;
@@ -411,7 +520,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t b_base = sw128_desc(su32(sb));
       const uint32_t a_step = (uint32_t)(stage_bytes >> 4);
       const uint32_t b_step = (uint32_t)(b_chunk >> 4);
-      int stage = 0;
+      int stage = 0, itile = 0;
       uint32_t ph = 0, bph = 0, tph = 0, buf = 0;
       for (int64_t it = pair; it < items; it += npairs) {
         const int64_t sp = it / p.set_tiles;
@@ -423,10 +532,29 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(bfull, bph);
           bph ^= 1;
         }
+        if constexpr (CG == 1) {
+          if (p.tstage) {
+            switch (p.ksteps) {
+#define EXEM_K4_ITEM(K)                                                       \
+  case K:                                                                     \
+    k4_item_tstage<K>(p, ntiles, stage, ph, tph, buf, itile, a_base, a_step, \
+                      b_base, b_step, tmem, full, empty, tfull, tempty);      \
+    break;
+              EXEM_K4_ITEM(1) EXEM_K4_ITEM(2) EXEM_K4_ITEM(3) EXEM_K4_ITEM(4)
+              EXEM_K4_ITEM(5) EXEM_K4_ITEM(6) EXEM_K4_ITEM(7)
+              default: EXEM_K4_ITEM(8)
+#undef EXEM_K4_ITEM
+            }
+            umma_commit(bempty);
+            continue;
+          }
+        }
         // acquire event 0 (accumulator buffer free + point chunk landed)
         mbar_wait(&tempty[buf], ((tph >> buf) & 1u) ^ 1u);
+        TRB(0, itile);
         tph ^= 1u << buf;
         mbar_wait(&full[stage], ph);
+        TRB(1, itile);
         fence_after();
         int kc = 0;
         for (int e = 0; e < nev; ++e) {
@@ -449,26 +577,38 @@ __global__ void __launch_bounds__(kThreads, 1)
             nstage = 0;
             nph ^= 1u;
           }
+          const bool trc = kc == 1 || (p.kchunks == 1);
+          if (trc) TRB(7, itile);
 #pragma unroll 1
           for (int j = 0; j < head; ++j)
             issue_mma<CG>(p, d, ad, bd, kc, j);
+          if (trc) TRB(8, itile);
           if (e + 1 < nev) {
             if (last) {
               const uint32_t nb = buf ^ 1u;
               mbar_wait(&tempty[nb], ((tph >> nb) & 1u) ^ 1u);
+              TRB(0, itile + 1);
               tph ^= 1u << nb;
             }
             mbar_wait(&full[nstage], nph);
-            fence_after();
+            if (last) TRB(1, itile + 1);
+            // the tcgen05 fence orders the next MMAs' TMEM writes after the
+            // epilogue's reads (tempty); smem data landed by TMA needs none
+            if (last) fence_after();
           }
+          if (trc) TRB(9, itile);
 #pragma unroll 1
           for (int j = head; j < nk; ++j)
             issue_mma<CG>(p, d, ad, bd, kc, j);
+          if (trc) TRB(10, itile);
           if constexpr (CG == 2) umma_commit_pair(&empty[stage]);
           else umma_commit(&empty[stage]);
+          if (trc) TRB(11, itile);
           if (last) {
             if constexpr (CG == 2) umma_commit_pair(&tfull[buf]);
             else umma_commit(&tfull[buf]);
+            TRB(2, itile);
+            ++itile;
             buf ^= 1u;
             kc = 0;
           } else {
@@ -580,6 +720,10 @@ int exem_tc_set_geometry(int64_t k_max, int32_t *spt, int32_t *w,
                 "(k_max=%lld)", (long long)k_max);
   int64_t s = 256 / ww;
   if (s > tcb::kMaxSpt) s = tcb::kMaxSpt;
+  if (const char *e = getenv("EXEM_TCB_SPT")) {  // timing experiments only
+    const int64_t f = atoll(e);
+    if (f >= 1 && f < s) s = f;
+  }
   *spt = (int32_t)s;
   *w = (int32_t)ww;
   *ncols = (int32_t)round_up(s * ww, 16);
@@ -665,12 +809,25 @@ int exem_batch_eval_tc(int dtype, const void *xp, int64_t n, const void *aux,
     prm.dbg = dbg ? atoi(dbg) : 0;
   }
   prm.partial = partial;
+  prm.trace = nullptr;
+  const char *trace_path = getenv("EXEM_TCB_TRACE");
+  if (trace_path) {
+    cudaMalloc(&prm.trace, 12 * kTrace * sizeof(long long));
+    cudaMemset(prm.trace, 0, 12 * kTrace * sizeof(long long));
+  }
   const int b_chunk = (nc / cg) * 128;
   const int avail = kSmemBudget - kBarBytes - 1024;
   // set tile stationary when it leaves room for >= 3 point-chunk stages
   const bool bstream = (avail - prm.kchunks * b_chunk) / A_CHUNK < 3;
   const int sb_bytes = bstream ? 0 : prm.kchunks * b_chunk;
-  const int stage_bytes = A_CHUNK + (bstream ? b_chunk : 0);
+  // whole-tile point stages (one handshake per tile) when >= 3 fit and the
+  // K loop unrolls (K <= 128); EXEM_TCB_DEBUG 128 disables (timing only)
+  const bool tstage = cg == 1 && !bstream && prm.ksteps <= 8 &&
+                      (avail - sb_bytes) / (prm.kchunks * A_CHUNK) >= 3 &&
+                      !(prm.dbg & 128);
+  prm.tstage = tstage ? 1 : 0;
+  const int stage_bytes = tstage ? prm.kchunks * A_CHUNK
+                                 : A_CHUNK + (bstream ? b_chunk : 0);
   int stages = (avail - sb_bytes) / stage_bytes;
   if (stages > 16) stages = 16;
   if (stages < 2) return fail(EXEM_ERR_UNSUPPORTED, "set tile too large for smem");
@@ -727,6 +884,18 @@ int exem_batch_eval_tc(int dtype, const void *xp, int64_t n, const void *aux,
   if (e != cudaSuccess)
     return fail(EXEM_ERR_CUDA, "batch_tc_kernel launch: %s",
                 cudaGetErrorString(e));
+  if (prm.trace) {  // timing experiment: dump the CTA-0 timeline
+    static long long host[12 * kTrace];
+    cudaStreamSynchronize((cudaStream_t)stream);
+    cudaMemcpy(host, prm.trace, sizeof(host), cudaMemcpyDeviceToHost);
+    cudaFree(prm.trace);
+    if (FILE *f = fopen(trace_path, "w")) {
+      for (int t = 0; t < kTrace; ++t)
+        for (int s2 = 0; s2 < 12; ++s2)
+          fprintf(f, "%lld%c", host[s2 * kTrace + t], s2 == 11 ? '\n' : ' ');
+      fclose(f);
+    }
+  }
   EXEM_LAUNCH_CHECK("batch_tc_kernel");
   return EXEM_OK;
 }

@@ -8,7 +8,7 @@ inputs (the parity contract of SURVEY.md 8(c) for the half paths):
 
 and the reference's own half bound (5e-2 vs binary32) through
 test_gpu_parity.py.  Geometry cases cover: one set per tile (k_max = 256),
-many sets per tile (k_max = 1 -> 32 sets of 8 columns), ragged
+many sets per tile (k_max = 1 -> 16 sets of 8 columns), ragged
 cardinalities (blank slots), l not a multiple of the sets per tile, n not a
 multiple of the 128-point tile with several partial-sum splits, the
 stationary set tile with whole / per-chunk point stages (d <= 256) and the
@@ -54,7 +54,7 @@ def _check(g, sets, vals, nref=None):
 @pytest.mark.parametrize("prec", [BF16, P16])
 @pytest.mark.parametrize("n,d,l,kmin,kmax", [
     (3000, 100, 150, 1, 50),      # ragged, 4 sets/tile of 56 columns
-    (1000, 2, 70, 1, 1),          # k_max = 1: 32 sets of 8 columns per tile
+    (1000, 2, 70, 1, 1),          # k_max = 1: 16 sets of 8 columns per tile
     (2500, 16, 45, 8, 8),         # exact multiple-of-8 sets
     (1300, 256, 20, 1, 256),      # one set per tile, per-chunk point stages
     (777, 700, 9, 3, 40),         # streamed set tile (d > stationary budget)

@@ -542,6 +542,17 @@ int run_pp(const char *name, int tiles) {
 
 int main(int argc, char **argv) {
   const int T = 4000, K = 7;
+  if (argc > 1 && argv[1][0] == 'c' && argv[1][1] == 'm') {  // commit cost
+    int dm = 1;
+    cudaMemcpyToSymbol(g_data, &dm, sizeof(int));
+    run<128, 256, 1, false>("cg1 N256 no commits", T, K);
+    run<128, 256, 1, false, true>("cg1 N256 commit/1", T, K, 1);
+    run<128, 256, 1, false, true>("cg1 N256 commit/2", T, K, 2);
+    run<128, 256, 1, false, true>("cg1 N256 commit/4", T, K, 4);
+    run<128, 256, 1, false, true>("cg1 N256 commit/7", T, K, 7);
+    run<128, 256, 1, false, true>("cg1 N256 commit/28", T, K, 28);
+    return 0;
+  }
   if (argc > 1) {  // cta_group::2 shapes only
     int dm = 1;
     cudaMemcpyToSymbol(g_data, &dm, sizeof(int));

@@ -13,6 +13,7 @@ from __future__ import annotations
 import argparse
 import csv
 import io
+import re
 import json
 import subprocess
 from collections import defaultdict
@@ -33,6 +34,7 @@ KEYS = [
     "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
     "sm__inst_executed_pipe_tma.sum",
     "smsp__issue_active.avg.pct_of_peak_sustained_active",
+    "l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
     "launch__registers_per_thread",
     "launch__shared_mem_per_block_dynamic",
     "launch__grid_size",
@@ -48,7 +50,12 @@ def raw_metrics(rep: Path) -> dict:
     res = {}
     for r in rows[2:]:
         name = r[hdr.index("Kernel Name")] if "Kernel Name" in hdr else "?"
-        m = {h: (v, u) for h, v, u in zip(hdr, r, units)}
+        # section-prefixed names (e.g. "TPC.TriageCompute.sm__...") are
+        # keyed by the bare metric name
+        m = {}
+        for h, v, u in zip(hdr, r, units):
+            mm = re.search(r"[a-z0-9]+__.*", h)
+            m[mm.group(0) if mm else h] = (v, u)
         res.setdefault(name, m)
     return res
 
@@ -60,7 +67,7 @@ def to_float(v: str) -> float:
         return float("nan")
 
 
-def summarise_rep(rep: Path, tag: str):
+def summarise_rep(rep: Path, tag: str, name_tag: str = "gains_tc"):
     mets = raw_metrics(rep)
     lines = [f"# ncu --set full: {rep.name} ({tag})", ""]
     traffic = None
@@ -80,12 +87,13 @@ def summarise_rep(rep: Path, tag: str):
             traffic = (to_float(rd[0]) * scale.get(rd[1], 1)
                        + to_float(wr[0]) * scale.get(wr[1], 1))
         lines.append("")
-    (ROOT / "profiles" / f"{tag}_gains_tc_ncu.md").write_text("\n".join(lines))
-    if traffic is not None:
+    (ROOT / "profiles" / f"{tag}_{name_tag}_ncu.md").write_text("\n".join(lines))
+    if traffic is not None and name_tag == "gains_tc":
         (ROOT / "profiles" / "gains_tc_traffic.json").write_text(json.dumps(
             {"bytes_per_launch": traffic, "source": f"profiles/{tag}_gains_tc_ncu.md",
              "note": "dram__bytes_read.sum + dram__bytes_write.sum of one "
-                     "gains_tc_kernel launch (ncu --set full, C4 step)"},
+                     "gains_tc_kernel launch (ncu --set full, C4 step)",
+             "n": 1000000, "d": 100, "world": 1},
             indent=1) + "\n")
     return traffic
 
@@ -118,9 +126,10 @@ def main():
     ap.add_argument("--rep")
     ap.add_argument("--launches")
     ap.add_argument("--tag", default="r01")
+    ap.add_argument("--name", default="gains_tc")
     a = ap.parse_args()
     if a.rep:
-        print("traffic bytes/launch:", summarise_rep(Path(a.rep), a.tag))
+        print("traffic bytes/launch:", summarise_rep(Path(a.rep), a.tag, a.name))
     if a.launches:
         summarise_launches(Path(a.launches), a.tag)
 
