@@ -77,6 +77,7 @@ struct BParams {
   int stages;          // point-chunk ring depth
   int bstream;         // 1: set chunks streamed with the point chunks
   int tstage;          // 1: a ring stage holds a whole point tile (all K)
+  int gch;             // otherwise: 64-wide K chunks per ring stage (1, 2)
   int dbg;             // timing experiments only (EXEM_TCB_DEBUG), 0 in use
   uint32_t idesc;
   long long *trace;    // timing experiments only (EXEM_TCB_TRACE): CTA-0 timeline
@@ -357,17 +358,19 @@ __device__ __forceinline__ void k4_item_tstage(
   }
 }
 
+// MMA j of an event whose stage holds consecutive 64-wide K chunks: chunk
+// j>>2 of the event, K=16 step j&3 inside the 128-B swizzle row.
 template <int CG>
 __device__ __forceinline__ void issue_mma(const BParams &p, uint32_t d,
-                                          uint64_t ad, uint64_t bd, int kc,
-                                          int j) {
+                                          uint64_t ad, uint64_t bd,
+                                          uint32_t b_step, int kc, int j) {
   if (p.dbg & 2) return;  // timing experiment: no MMA
+  const uint64_t a = ad + (uint64_t)((j >> 2) * (A_CHUNK >> 4) + (j & 3) * 2);
+  const uint64_t b = bd + (uint64_t)((j >> 2) * b_step + (j & 3) * 2);
   if constexpr (CG == 2)
-    umma_f16_pair(d, ad + (uint64_t)(2 * j), bd + (uint64_t)(2 * j), p.idesc,
-                  (kc | j) ? 1u : 0u);
+    umma_f16_pair(d, a, b, p.idesc, (kc | j) ? 1u : 0u);
   else
-    umma_f16(d, ad + (uint64_t)(2 * j), bd + (uint64_t)(2 * j), p.idesc,
-             (kc | j) ? 1u : 0u);
+    umma_f16(d, a, b, p.idesc, (kc | j) ? 1u : 0u);
 }
 
 template <int CG>
@@ -382,7 +385,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int b_chunk = bh * 128;       // bytes of one set-tile K-chunk half
   const int sb_bytes = p.bstream ? 0 : p.kchunks * b_chunk;
   const int stage_bytes = p.tstage ? p.kchunks * A_CHUNK
-                                   : A_CHUNK + (p.bstream ? b_chunk : 0);
+                                   : p.gch * A_CHUNK + (p.bstream ? b_chunk : 0);
   unsigned char *sb = smem;                        // stationary set tile
   unsigned char *sa = smem + sb_bytes;             // point-chunk ring
   uint64_t *bars = (uint64_t *)(sa + p.stages * stage_bytes);
@@ -482,28 +485,34 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int64_t pt = p0; pt < p1 && !p.tstage; pt += BM * CG, ++ptile) {
           const int prow = (int)(pt + BM * rank);
-          for (int kc = 0; kc < p.kchunks; ++kc) {
+          for (int kc = 0; kc < p.kchunks; kc += p.gch) {
+            const int gn = p.kchunks - kc < p.gch ? p.kchunks - kc : p.gch;
             mbar_wait_sleep(&empty[stage], ph ^ 1);
             if (kc == 0) TRB(5, ptile);
             unsigned char *dst = sa + stage * stage_bytes;
             if (p.dbg & 4) {  // timing experiment: no point-operand traffic
               if (rank == 0) mbar_arrive(&full[stage]);
             } else {
-              if (rank == 0)
-                mbar_expect_tx(&full[stage], (uint32_t)(CG * stage_bytes));
+              const uint32_t bytes =
+                  (uint32_t)(gn * A_CHUNK + (p.bstream ? b_chunk : 0));
+              if (rank == 0) mbar_expect_tx(&full[stage], (uint32_t)CG * bytes);
               if constexpr (CG == 2) {
                 const uint32_t fc = mapa(&full[stage], 0);
-                tma_load_2d_pair(dst, &map_p, fc, kc * KCH, prow);
+                for (int j = 0; j < gn; ++j)
+                  tma_load_2d_pair(dst + j * A_CHUNK, &map_p, fc,
+                                   (kc + j) * KCH, prow);
                 if (p.bstream)
                   tma_load_2d_pair(dst + A_CHUNK, &map_s, fc, kc * KCH, srow);
               } else {
-                tma_load_2d(dst, &map_p, &full[stage], kc * KCH, prow);
+                for (int j = 0; j < gn; ++j)
+                  tma_load_2d(dst + j * A_CHUNK, &map_p, &full[stage],
+                              (kc + j) * KCH, prow);
                 if (p.bstream)
                   tma_load_2d(dst + A_CHUNK, &map_s, &full[stage], kc * KCH,
                               srow);
               }
             }
-            if (kc == p.kchunks - 1) TRB(6, ptile);
+            if (kc + gn >= p.kchunks) TRB(6, ptile);
             if (++stage == p.stages) {
               stage = 0;
               ph ^= 1;
@@ -527,7 +536,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int64_t p0 = sp * p.split_pts;
         const int64_t p1 = min(p.n, p0 + p.split_pts);
         const int ntiles = (int)((p1 - p0 + BM * CG - 1) / (BM * CG));
-        const int nev = ntiles * p.kchunks;
+        const int kev = (p.kchunks + p.gch - 1) / p.gch;  // events per tile
+        const int nev = ntiles * kev;
         if (!p.bstream) {
           mbar_wait(bfull, bph);
           bph ^= 1;
@@ -563,14 +573,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint64_t bd = p.bstream ? ad + (uint64_t)(A_CHUNK >> 4)
                                         : b_base + (uint64_t)(kc * b_step);
           const int rem = p.ksteps - kc * 4;
-          const int nk = rem < 4 ? rem : 4;
+          const int nk = rem < 4 * p.gch ? rem : 4 * p.gch;
           // acquisitions for event e+1 (accumulator buffer when e+1 starts a
           // tile, then its point chunk) hide behind this chunk's last two
           // queued MMAs.  (Splitting them -- B stage before MMA nk-2, buffer
           // before nk-1, the better placement for K3 -- measured 1.5x
           // slower here: profiles/r01_k4_probe.log.)
           const int head = nk > 2 ? nk - 2 : 0;
-          const bool last = (kc == p.kchunks - 1);
+          const bool last = (kc + p.gch >= p.kchunks);
           int nstage = stage + 1;
           uint32_t nph = ph;
           if (nstage == p.stages) {
@@ -581,7 +591,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (trc) TRB(7, itile);
 #pragma unroll 1
           for (int j = 0; j < head; ++j)
-            issue_mma<CG>(p, d, ad, bd, kc, j);
+            issue_mma<CG>(p, d, ad, bd, b_step, kc, j);
           if (trc) TRB(8, itile);
           if (e + 1 < nev) {
             if (last) {
@@ -599,7 +609,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (trc) TRB(9, itile);
 #pragma unroll 1
           for (int j = head; j < nk; ++j)
-            issue_mma<CG>(p, d, ad, bd, kc, j);
+            issue_mma<CG>(p, d, ad, bd, b_step, kc, j);
           if (trc) TRB(10, itile);
           if constexpr (CG == 2) umma_commit_pair(&empty[stage]);
           else umma_commit(&empty[stage]);
@@ -612,7 +622,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             buf ^= 1u;
             kc = 0;
           } else {
-            ++kc;
+            kc += p.gch;
           }
           stage = nstage;
           ph = nph;
@@ -826,8 +836,16 @@ int exem_batch_eval_tc(int dtype, const void *xp, int64_t n, const void *aux,
                       (avail - sb_bytes) / (prm.kchunks * A_CHUNK) >= 3 &&
                       !(prm.dbg & 128);
   prm.tstage = tstage ? 1 : 0;
+  // otherwise two K chunks per stage when >= 2 such stages fit: half the
+  // per-stage handshakes (d = 256: 149 -> 134 ms with only 2 stages,
+  // profiles/r01_k4_probe.log); EXEM_TCB_G forces 1 or 2 (experiments)
+  int gch = (!tstage && !bstream && prm.kchunks >= 2 &&
+             (avail - sb_bytes) / (2 * A_CHUNK) >= 2) ? 2 : 1;
+  if (const char *e = getenv("EXEM_TCB_G"))
+    if (!tstage && !bstream) gch = atoi(e) == 2 && prm.kchunks >= 2 ? 2 : 1;
+  prm.gch = gch;
   const int stage_bytes = tstage ? prm.kchunks * A_CHUNK
-                                 : A_CHUNK + (bstream ? b_chunk : 0);
+                                 : gch * A_CHUNK + (bstream ? b_chunk : 0);
   int stages = (avail - sb_bytes) / stage_bytes;
   if (stages > 16) stages = 16;
   if (stages < 2) return fail(EXEM_ERR_UNSUPPORTED, "set tile too large for smem");
