@@ -202,6 +202,23 @@ int exem_batch_eval_tc(int dtype, const void *xp, int64_t n, const void *aux,
                        int64_t split_pts, double *partial, int64_t splits,
                        void *stream);
 
+/*
+ * Binary32 on tensor cores (split-bf16): each fp32 coordinate is split into
+ * three bf16 pieces and the pieces are laid out along K (6d columns, then
+ * the folded constants) so that exem_greedy_gains_tc with d' =
+ * exem_tc_split_dim(d) computes the K3 gains at binary32 accuracy
+ * (all piece products with i+j <= 2, each exact in fp32).
+ *   role 0: candidate rows from vt/norms; role 1: point rows from vt/norms/m.
+ *   exem_tc_refresh_h rewrites the three -h columns (at hcol = 6d) of point
+ *   rows from norms and an updated m (after exem_greedy_update).
+ */
+int64_t exem_tc_split_dim(int64_t d);
+int exem_tc_pack_split(int role, const void *vt, int64_t ld, int64_t n,
+                       int64_t d, const double *norms, const void *m,
+                       void *x, void *stream);
+int exem_tc_refresh_h(const double *norms, const void *m, int64_t n, void *x,
+                      int64_t kp, int64_t hcol, void *stream);
+
 /* Build the TC candidate operand from the SIMT layout (+ norms). */
 int exem_tc_pack_candidates(int dtype, const void *vt, int64_t ld, int64_t n,
                             int64_t d, const double *norms, void *xc,

@@ -82,6 +82,10 @@ _SIGNATURES = {
     "exem_sum_fixed": (c_int, [_P, c_int64, _P, c_int64, _P]),
     "exem_pack_elements": (c_int, [c_int, _P, _P, _P, c_int64, c_int64,
                                    c_int64, c_int64, _P, _P]),
+    "exem_tc_split_dim": (c_int64, [c_int64]),
+    "exem_tc_pack_split": (c_int, [c_int, _P, c_int64, c_int64, c_int64, _P,
+                                   _P, _P, _P]),
+    "exem_tc_refresh_h": (c_int, [_P, _P, c_int64, _P, c_int64, c_int64, _P]),
     "exem_launch_count": (c_int64, []),
 }
 

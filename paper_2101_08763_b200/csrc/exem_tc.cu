@@ -577,6 +577,85 @@ __global__ void pack_kernel(const float *__restrict__ vt, int64_t ld,
 }
 
 
+// ------------------------------------------- split-bf16 binary32 operands
+// An fp32 value x is split into three bf16 pieces x0 + x1 + x2 (x0 = bf16(x),
+// x1 = bf16(x - x0), x2 = bf16(x - x0 - x1): 24 significant bits, exact for
+// binary32).  Laying the pieces out along K as
+//   candidate row  [c0, c0, c1, c0, c1, c2, 1,1,1, -b0,-b1,-b2, 0..]
+//   point row      [v0, v1, v0, v2, v1, v0, -h0,-h1,-h2, 1,1,1, 0..]
+// makes one bf16 row-dot over K' = 6d+6 equal to
+//   c.v (all piece products with i+j <= 2; each is exact in fp32, the dropped
+//   ones are < 2^-24 relative) - h - b,
+// i.e. the K3 quantity D at binary32 accuracy on the tensor cores: the
+// unchanged gains_tc_kernel runs on these rows with "d" = 6d.
+__device__ __forceinline__ void split3(float x, __nv_bfloat16 (&o)[3]) {
+  o[0] = __float2bfloat16_rn(x);
+  const float r1 = x - __bfloat162float(o[0]);
+  o[1] = __float2bfloat16_rn(r1);
+  o[2] = __float2bfloat16_rn(r1 - __bfloat162float(o[1]));
+}
+
+template <bool kCand>
+__global__ void pack_split3_kernel(const float *__restrict__ vt, int64_t ld,
+                                   int64_t n, int d,
+                                   const double *__restrict__ norms,
+                                   const float *__restrict__ m,
+                                   __nv_bfloat16 *__restrict__ x, int64_t kp,
+                                   int64_t rows) {
+  // piece order of the six d-wide segments (see above)
+  constexpr int kCandPiece[6] = {0, 0, 1, 0, 1, 2};
+  constexpr int kPointPiece[6] = {0, 1, 0, 2, 1, 0};
+  const int64_t r = (int64_t)blockIdx.x * blockDim.y + threadIdx.y;
+  if (r >= rows) return;
+  __nv_bfloat16 *row = x + r * kp;
+  const __nv_bfloat16 zero = __float2bfloat16_rn(0.f);
+  for (int64_t k = threadIdx.x; k < kp; k += blockDim.x) {
+    __nv_bfloat16 v = zero;
+    if (r < n) {
+      if (k < 6 * (int64_t)d) {
+        const int seg = (int)(k / d), dim = (int)(k % d);
+        __nv_bfloat16 pc[3];
+        split3(vt[(int64_t)dim * ld + r], pc);
+        v = pc[kCand ? kCandPiece[seg] : kPointPiece[seg]];
+      } else if (k < 6 * (int64_t)d + kTcConst) {
+        const int c = (int)(k - 6 * (int64_t)d);
+        const bool ones = kCand ? (c < 3) : (c >= 3);
+        if (ones) {
+          v = __float2bfloat16_rn(1.f);
+        } else {
+          const double t = kCand ? 0.5 * norms[r]
+                                 : 0.5 * (norms[r] - (m ? (double)m[r] : 0.0));
+          const double t0 = (double)__bfloat162float(__double2bfloat16(t));
+          const double t1 = (double)__bfloat162float(__double2bfloat16(t - t0));
+          const double t2 =
+              (double)__bfloat162float(__double2bfloat16(t - t0 - t1));
+          const int piece = kCand ? c - 3 : c;
+          v = __double2bfloat16(-(piece == 0 ? t0 : (piece == 1 ? t1 : t2)));
+        }
+      }
+    }
+    row[k] = v;
+  }
+}
+
+// Rewrite only the three -h columns (at column hcol) of point rows after an
+// m-update: h_i = (||v_i||^2 - m_i)/2 in three bf16 pieces.
+__global__ void refresh_h_kernel(const double *__restrict__ norms,
+                                 const float *__restrict__ m, int64_t n,
+                                 __nv_bfloat16 *__restrict__ x, int64_t kp,
+                                 int64_t hcol) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double h = 0.5 * (norms[i] - (double)m[i]);
+  const double t0 = (double)__bfloat162float(__double2bfloat16(h));
+  const double t1 = (double)__bfloat162float(__double2bfloat16(h - t0));
+  const double t2 = (double)__bfloat162float(__double2bfloat16(h - t0 - t1));
+  __nv_bfloat16 *row = x + i * kp + hcol;
+  row[0] = __double2bfloat16(-t0);
+  row[1] = __double2bfloat16(-t1);
+  row[2] = __double2bfloat16(-t2);
+}
+
 }  // namespace tc
 }  // namespace exem
 
@@ -720,6 +799,38 @@ int exem_greedy_gains_tc(int dtype, const void *xc, int64_t l, const void *xp,
       fclose(f);
     }
   }
+  return EXEM_OK;
+}
+
+int64_t exem_tc_split_dim(int64_t d) { return 6 * d; }
+
+int exem_tc_pack_split(int role, const void *vt, int64_t ld, int64_t n,
+                       int64_t d, const double *norms, const void *m,
+                       void *x, void *stream) {
+  if (n < 1 || d < 1) return fail(EXEM_ERR_ARG, "tc_pack_split: bad shape");
+  const int64_t kp = exem_tc_kp(6 * d), rows = exem_tc_rows(n);
+  dim3 block(64, 4);
+  dim3 grid((unsigned)ceil_div(rows, 4));
+  cudaStream_t st = (cudaStream_t)stream;
+  if (role == 0)
+    tc::pack_split3_kernel<true><<<grid, block, 0, st>>>(
+        (const float *)vt, ld, n, (int)d, norms, nullptr, (__nv_bfloat16 *)x,
+        kp, rows);
+  else
+    tc::pack_split3_kernel<false><<<grid, block, 0, st>>>(
+        (const float *)vt, ld, n, (int)d, norms, (const float *)m,
+        (__nv_bfloat16 *)x, kp, rows);
+  EXEM_LAUNCH_CHECK("tc_pack_split");
+  return EXEM_OK;
+}
+
+int exem_tc_refresh_h(const double *norms, const void *m, int64_t n, void *x,
+                      int64_t kp, int64_t hcol, void *stream) {
+  if (n < 1) return EXEM_OK;
+  tc::refresh_h_kernel<<<(unsigned)ceil_div(n, 256), 256, 0,
+                         (cudaStream_t)stream>>>(
+      norms, (const float *)m, n, (__nv_bfloat16 *)x, kp, hcol);
+  EXEM_LAUNCH_CHECK("tc_refresh_h");
   return EXEM_OK;
 }
 

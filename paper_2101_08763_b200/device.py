@@ -128,6 +128,19 @@ class DeviceGround:
                                N.ptr(self._xp0), self.stream)
         return self._xp0
 
+    def xc_split(self):
+        """Split-bf16 binary32 candidate operand (exem_tc_pack_split)."""
+        if getattr(self, "_xcs", None) is None:
+            t = torch()
+            lib = N.lib()
+            rows = int(lib.tc_rows(self.n))
+            kp = int(lib.tc_kp(int(lib.tc_split_dim(self.d))))
+            self._xcs = t.empty((rows, kp), dtype=t.bfloat16, device=self.dev)
+            lib.tc_pack_split(0, N.ptr(self.vt), self.ld, self.n, self.d,
+                              N.ptr(self.norms), None, N.ptr(self._xcs),
+                              self.stream)
+        return self._xcs
+
     def xc(self):
         """Tensor-core candidate operand [tc_rows][kp] (built once)."""
         if self._xc is None:

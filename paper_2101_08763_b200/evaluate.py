@@ -57,6 +57,9 @@ class Evaluator:
     worker_count: int = 1
     precision: Optional[Precision] = None
     device: Optional[int] = None
+    # binary32 Greedy gains on the tensor cores via split-bf16 operands
+    # (opt-in; the default binary32 path is the CUDA-core K3-SIMT)
+    tensor_fp32: bool = False
 
     def __post_init__(self):
         if self.backend not in BACKENDS:

@@ -48,6 +48,7 @@ from .objective import (
 )
 
 BRUTE_FORCE_LIMIT = 10**6
+SPLIT32_MAX_D = 128
 
 
 @dataclass(frozen=True)
@@ -68,7 +69,7 @@ class GreedyRun:
     """
 
     def __init__(self, dg, cand=None, k_cap: int = 1, split_pts=None,
-                 tc: Optional[bool] = None):
+                 tc: Optional[bool] = None, split32: bool = False):
         from .device import torch
 
         t = torch()
@@ -78,6 +79,15 @@ class GreedyRun:
         self.cand = cand or dg
         self.prec = dg.precision
         self.tc = self.prec.is_half if tc is None else tc
+        # binary32 gains on the tensor cores through split-bf16 operands
+        # (exem_tc_pack_split): the K3-TC kernel with d' = 6d
+        # (d <= 128: beyond, the tensor core's fp32 accumulation over
+        # K' = 6d + 6 terms exceeds the binary32 tolerance on the gains --
+        # measured 1.09e-5 at d = 256 -- so larger d keeps the SIMT path)
+        self.split32 = (bool(split32) and self.prec.tag == N.F32 and
+                        dg.d <= SPLIT32_MAX_D)
+        if self.split32:
+            self.tc = True
         self.split_pts = int(split_pts or dg.split_pts)
         self.splits = -(-dg.n // self.split_pts)
         self.l = self.cand.n
@@ -94,7 +104,17 @@ class GreedyRun:
         self._partial = None
         self.xp = None
         self.xc = None
-        if self.tc:
+        self.tc_tag = self.prec.tag
+        self.tc_d = dg.d
+        if self.split32:
+            self.tc_tag = N.BF16
+            self.tc_d = int(self.lib.tc_split_dim(dg.d))
+            self.kp = int(self.lib.tc_kp(self.tc_d))
+            rows = int(self.lib.tc_rows(dg.n))
+            self.xp = t.empty((rows, self.kp), dtype=t.bfloat16, device=dev)
+            self.xc = self.cand.xc_split()
+        elif self.tc:
+            self.kp = dg.kp
             rows = int(self.lib.tc_rows(dg.n))
             tdt = t.bfloat16 if self.prec.tag == N.BF16 else t.float16
             self.xp = t.empty((rows, dg.kp), dtype=tdt, device=dev)
@@ -116,7 +136,11 @@ class GreedyRun:
         dg, lib = self.dg, self.lib
         lib.greedy_init(self.prec.tag, N.ptr(dg.aux), dg.n, N.ptr(self.m),
                         N.ptr(self.msum0), N.ptr(self.scratch), self.stream)
-        if self.tc:
+        if self.split32:
+            lib.tc_pack_split(1, N.ptr(dg.vt), dg.ld, dg.n, dg.d,
+                              N.ptr(dg.norms), N.ptr(self.m), N.ptr(self.xp),
+                              self.stream)
+        elif self.tc:
             lib.tc_pack_points(self.prec.tag, N.ptr(dg.vt), dg.ld, dg.n, dg.d,
                                N.ptr(dg.norms), N.ptr(self.m), N.ptr(self.xp),
                                self.stream)
@@ -131,10 +155,10 @@ class GreedyRun:
             part = self.partial(cl)
             if self.tc:
                 xc_ptr = N.c_void_p(self.xc.data_ptr() +
-                                    c0 * cd.kp * self.xc.element_size())
-                lib.greedy_gains_tc(self.prec.tag, xc_ptr, cl, N.ptr(self.xp),
-                                    dg.n, dg.d, self.split_pts, N.ptr(part),
-                                    self.splits, st)
+                                    c0 * self.kp * self.xc.element_size())
+                lib.greedy_gains_tc(self.tc_tag, xc_ptr, cl, N.ptr(self.xp),
+                                    dg.n, self.tc_d, self.split_pts,
+                                    N.ptr(part), self.splits, st)
             else:
                 cvt_ptr = N.c_void_p(cd.vt.data_ptr() + c0 * esz)
                 cn_ptr = N.c_void_p(cd.norms.data_ptr() + c0 * 8)
@@ -159,8 +183,12 @@ class GreedyRun:
         self.lib.greedy_update(
             self.prec.tag, N.ptr(dg.vt), dg.ld, dg.n, dg.d, N.ptr(dg.norms),
             N.ptr(cd.vt), cd.ld, N.ptr(cd.norms), N.ptr(self.sel_idx), step,
-            N.ptr(self.m), N.ptr(self.xp), dg.kp, N.ptr(self.msum),
-            N.ptr(self.scratch), self.stream)
+            N.ptr(self.m), None if self.split32 else N.ptr(self.xp), dg.kp,
+            N.ptr(self.msum), N.ptr(self.scratch), self.stream)
+        if self.split32:
+            self.lib.tc_refresh_h(N.ptr(dg.norms), N.ptr(self.m), dg.n,
+                                  N.ptr(self.xp), self.kp, self.tc_d,
+                                  self.stream)
 
     def step(self, step: int, chunk: Optional[int] = None):
         self.compute_gains(chunk)
@@ -214,7 +242,7 @@ def greedy_maximize(ground: GroundSet, k: int,
     from .device import torch
 
     with torch().cuda.device(dg.device_index):
-        run = GreedyRun(dg, k_cap=k)
+        run = GreedyRun(dg, k_cap=k, split32=evaluator.tensor_fp32)
         run.start()
         for step in range(k):
             run.step(step, _chunk_for_budget(ground, step, memory_budget))

@@ -67,7 +67,7 @@ def timed(fn, stream, reps=3):
     return float(np.median(ts))
 
 
-def greedy_case(n, d, prec_name, picks, seed, pk):
+def greedy_case(n, d, prec_name, picks, seed, pk, split32=False):
     """Run `picks` real Greedy steps, then time the next step's K3 launch."""
     import torch
 
@@ -79,7 +79,7 @@ def greedy_case(n, d, prec_name, picks, seed, pk):
     V = np.random.default_rng(seed).standard_normal((n, d), dtype=np.float32)
     g = pb.build_ground_set(V, precision=prec)
     dg = g.on_device(0)
-    run = GreedyRun(dg, k_cap=picks + 1)
+    run = GreedyRun(dg, k_cap=picks + 1, split32=split32)
     run.start()
     for s in range(picks):
         run.step(s)
@@ -94,10 +94,12 @@ def greedy_case(n, d, prec_name, picks, seed, pk):
     l = n - picks
     flop = 2.0 * n * l * d
     lib = N.lib()
-    if prec.is_half:
+    if prec.is_half or run.split32:
         kexec = int(-(-(d + 6) // 16) * 16)
+        if run.split32:
+            kexec = int(-(-(6 * d + 6) // 16) * 16)
         pipe, peak = "tensor", pk["bf16"]
-        kern = "gains_tc_kernel"
+        kern = "gains_tc_kernel" + (" (split-bf16 fp32)" if run.split32 else "")
     else:
         kexec = int(lib.pad_dims(d))
         pipe = "fp64-pipe" if prec_name == "fp64" else "fp32-pipe"
@@ -176,6 +178,7 @@ def main():
 
     if "c2" in only:
         emit("C2", greedy_case(args.n, 100, "fp32", 19, 0, pk))
+        emit("C2", greedy_case(args.n, 100, "fp32", 19, 0, pk, split32=True))
     if "c3" in only:
         for d in [int(x) for x in args.dims.split(",")]:
             for p in args.precs.split(","):
