@@ -294,6 +294,22 @@ int exem_packed_norms(int dtype, const void *packed, int64_t d, int64_t k_max,
 int exem_row_norms(int dtype, const void *x, int64_t rows, int64_t d,
                    int64_t d_pad, double *out, void *stream);
 
+/*
+ * Sieve streaming (north star: "the Greedy and streaming optimizers"; the
+ * reference ships none, SPEC.md:9,402 -- see sieve.py).  Each sieve s keeps
+ * an m-vector M[s][0..n) (row stride ldm) = per-point minimum over its set
+ * and aux.  For one arriving element with dist[i] = d(v_i, e) (exem_set_min
+ * with k = 1, include_aux = 0):
+ *   exem_sieve_gains   gains[s] = sum_i max(0, M[s][i] - dist[i]) (fixed
+ *                      order; scratch >= ceil(n/256) * sieves doubles)
+ *   exem_sieve_update  m <- min(m, dist) for one sieve row; msum[0] = sum m
+ */
+int exem_sieve_gains(int dtype, const void *M, int64_t ldm, int64_t sieves,
+                     const void *dist, int64_t n, double *gains,
+                     double *scratch, void *stream);
+int exem_sieve_update(int dtype, void *m, const void *dist, int64_t n,
+                      double *msum, double *scratch, void *stream);
+
 /* Number of kernels this library launched since load (evidence counter). */
 int64_t exem_launch_count(void);
 

@@ -86,6 +86,9 @@ _SIGNATURES = {
     "exem_tc_pack_split": (c_int, [c_int, _P, c_int64, c_int64, c_int64, _P,
                                    _P, _P, _P]),
     "exem_tc_refresh_h": (c_int, [_P, _P, c_int64, _P, c_int64, c_int64, _P]),
+    "exem_sieve_gains": (c_int, [c_int, _P, c_int64, c_int64, _P, c_int64,
+                                 _P, _P, _P]),
+    "exem_sieve_update": (c_int, [c_int, _P, _P, c_int64, _P, _P, _P]),
     "exem_launch_count": (c_int64, []),
 }
 

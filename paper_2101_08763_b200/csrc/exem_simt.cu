@@ -188,6 +188,44 @@ __global__ void __launch_bounds__(kRedThreads)
   if (threadIdx.x == 0) partials[blockIdx.x] = r;
 }
 
+// ============================================================ sieve kernels
+// Streaming (Sieve) optimizers keep one m-vector per sieve: M[s][i] =
+// min(aux_i, min_{e in S_s} d(v_i, e)).  For an arriving element with
+// distances dist[i] = d(v_i, e):
+//   sieve_gains:  partial[s][b] = sum_{i in block b} max(0, M[s][i] - dist[i])
+//   sieve_update: M[s][i] <- min(M[s][i], dist[i]); partial[b] = block sum
+// (fixed-order block partials, reduced by exem_reduce_partials /
+// exem_sum_fixed -> deterministic).
+template <typename C>
+__global__ void __launch_bounds__(kRedThreads)
+    sieve_gains_kernel(const C *__restrict__ M, int64_t ldm,
+                       const C *__restrict__ dist, int64_t n,
+                       double *__restrict__ partial, int64_t nblocks) {
+  __shared__ double sh[32];
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t s = blockIdx.y;
+  double v = 0.0;
+  if (i < n) v = (double)tmax(M[s * ldm + i] - dist[i], C(0));
+  const double r = block_sum<kRedThreads>(v, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x * gridDim.y + s] = r;
+}
+
+template <typename C>
+__global__ void __launch_bounds__(kRedThreads)
+    sieve_update_kernel(C *__restrict__ m, const C *__restrict__ dist,
+                        int64_t n, double *__restrict__ partials) {
+  __shared__ double sh[32];
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double v = 0.0;
+  if (i < n) {
+    const C mi = tmin(m[i], dist[i]);
+    m[i] = mi;
+    v = (double)mi;
+  }
+  const double r = block_sum<kRedThreads>(v, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = r;
+}
+
 // ============================================================ K2 greedy update
 // m_i <- min(m_i, d(v_i, c*)), c* read from sel_idx[step] on device.
 // Optionally refreshes the TC point operand's folded -h columns.
@@ -1009,6 +1047,40 @@ int exem_pack_elements(int dtype, const void *rows, const int64_t *offsets,
     EXEM_LAUNCH_CHECK("pack_elements_kernel");
   });
   return EXEM_OK;
+}
+
+int exem_sieve_gains(int dtype, const void *M, int64_t ldm, int64_t sieves,
+                     const void *dist, int64_t n, double *gains,
+                     double *scratch, void *stream) {
+  if (n < 1 || sieves < 1 || ldm < n)
+    return fail(EXEM_ERR_ARG, "sieve_gains: bad shape");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t blocks = ceil_div(n, kRedThreads);
+  dim3 grid((unsigned)blocks, (unsigned)sieves);
+  if (dtype == EXEM_F64)
+    sieve_gains_kernel<double><<<grid, kRedThreads, 0, st>>>(
+        (const double *)M, ldm, (const double *)dist, n, scratch, blocks);
+  else
+    sieve_gains_kernel<float><<<grid, kRedThreads, 0, st>>>(
+        (const float *)M, ldm, (const float *)dist, n, scratch, blocks);
+  EXEM_LAUNCH_CHECK("sieve_gains_kernel");
+  // scratch is [blocks][sieves]: the fixed-order column sums are the gains
+  return exem_reduce_partials(scratch, blocks, sieves, 1.0, gains, stream);
+}
+
+int exem_sieve_update(int dtype, void *m, const void *dist, int64_t n,
+                      double *msum, double *scratch, void *stream) {
+  if (n < 1) return fail(EXEM_ERR_ARG, "sieve_update: bad shape");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t blocks = ceil_div(n, kRedThreads);
+  if (dtype == EXEM_F64)
+    sieve_update_kernel<double><<<(unsigned)blocks, kRedThreads, 0, st>>>(
+        (double *)m, (const double *)dist, n, scratch);
+  else
+    sieve_update_kernel<float><<<(unsigned)blocks, kRedThreads, 0, st>>>(
+        (float *)m, (const float *)dist, n, scratch);
+  EXEM_LAUNCH_CHECK("sieve_update_kernel");
+  return reduce_fixed(scratch, blocks, msum, 0, st);
 }
 
 }  // extern "C"
