@@ -196,11 +196,23 @@ int exem_tc_set_geometry(int64_t k_max, int32_t *spt, int32_t *w,
 int64_t exem_tc_set_rows(int64_t l, int64_t k_max);
 int exem_tc_pack_sets(int dtype, const void *packed, const double *pnorms,
                       const int32_t *card, int64_t l, int64_t l_pad,
-                      int64_t k_max, int64_t d, void *xs, void *stream);
+                      int64_t k_max, int64_t d, void *xs, float *bs,
+                      void *stream);
 int exem_batch_eval_tc(int dtype, const void *xp, int64_t n, const void *aux,
-                       const void *xs, int64_t l, int64_t k_max, int64_t d,
-                       int64_t split_pts, double *partial, int64_t splits,
-                       void *stream);
+                       const double *norms, const void *xs, const float *bs,
+                       int64_t l, int64_t k_max, int64_t d, int64_t split_pts,
+                       double *partial, int64_t splits, void *stream);
+/* Plain (unfolded) K4-TC operands, used when folding the six constant
+ * columns would add a whole 64-wide K chunk (exem_tc_batch_plain(d) = 1,
+ * e.g. d = 256): point rows [v, 0..] and set rows [e, 0..] with stride
+ * exem_tc_batch_kp(d) = round_up(d, 64); exem_tc_pack_sets with bs != NULL
+ * writes plain set rows and bs[row] = ||e||^2/2, and exem_batch_eval_tc with
+ * bs != NULL adds the constants in the epilogue from bs and norms
+ * (min_e d = ||v||^2 - 2 max_e (v.e - ||e||^2/2)). */
+int64_t exem_tc_batch_plain(int64_t d);
+int64_t exem_tc_batch_kp(int64_t d);
+int exem_tc_pack_points_plain(int dtype, const void *vt, int64_t ld,
+                              int64_t n, int64_t d, void *xp, void *stream);
 
 /*
  * Binary32 on tensor cores (split-bf16): each fp32 coordinate is split into

@@ -71,10 +71,14 @@ _SIGNATURES = {
     "exem_tc_set_geometry": (c_int, [c_int64, _P, _P, _P]),
     "exem_tc_set_rows": (c_int64, [c_int64, c_int64]),
     "exem_tc_pack_sets": (c_int, [c_int, _P, _P, _P, c_int64, c_int64,
-                                  c_int64, c_int64, _P, _P]),
-    "exem_batch_eval_tc": (c_int, [c_int, _P, c_int64, _P, _P, c_int64,
-                                   c_int64, c_int64, c_int64, _P, c_int64,
-                                   _P]),
+                                  c_int64, c_int64, _P, _P, _P]),
+    "exem_batch_eval_tc": (c_int, [c_int, _P, c_int64, _P, _P, _P, _P,
+                                   c_int64, c_int64, c_int64, c_int64, _P,
+                                   c_int64, _P]),
+    "exem_tc_batch_plain": (c_int64, [c_int64]),
+    "exem_tc_batch_kp": (c_int64, [c_int64]),
+    "exem_tc_pack_points_plain": (c_int, [c_int, _P, c_int64, c_int64,
+                                          c_int64, _P, _P]),
     "exem_host_register": (c_int, [_P, c_int64]),
     "exem_host_unregister": (c_int, [_P]),
     "exem_h2d_rows": (c_int, [_P, _P, c_int64, c_int64, c_int64, c_int64,

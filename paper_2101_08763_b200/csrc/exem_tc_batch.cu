@@ -46,7 +46,7 @@ constexpr int kThreads = 320;
 constexpr int kEpiWarps = 8;
 constexpr int kMaxSpt = 16;             // sets per set tile (register budget of the epilogue)
 constexpr int kSmemBudget = 227 * 1024;
-constexpr int kBarBytes = 2048;
+constexpr int kBarBytes = 3072;  // barriers, reductions, plain b
 constexpr int kTrace = 256;  // tiles traced on CTA 0
 // CTA-0 timeline for timing experiments (tools/tcb_trace.py): compiled in
 // only with -DEXEM_TCB_TRACE_BUILD (EXEM_NVCC_FLAGS at build time) -- the
@@ -82,6 +82,9 @@ struct BParams {
   uint32_t idesc;
   long long *trace;    // timing experiments only (EXEM_TCB_TRACE): CTA-0 timeline
   const float *aux;    // [n] aux distances (compute type)
+  int plain;           // 1: unfolded operands, constants added in the epilogue
+  const double *norms; // plain: [n] ||v_i||^2
+  const float *bs;     // plain: [set rows] ||e||^2 / 2 per set-tile row
   double *partial;     // [splits][l]
 };
 
@@ -121,29 +124,39 @@ struct EpiShape {
   static constexpr int SPT = 32 / W8 < kMaxSpt ? 32 / W8 : kMaxSpt;
   static constexpr int MAXS = (SPT + 1) / 2;  // sets per warp (max)
   // sets per load batch: registers of one batch (8 per group) plus the fp64
-  // accumulators within a 120-register budget (ptxas caps this kernel at
+  // accumulators within a 116-register budget (ptxas caps this kernel at
   // 168 registers per thread)
   static constexpr int sb() {
     int best = 1;
     for (int s = 1; s <= MAXS; ++s)
-      if (s * W8 * 8 + 2 * MAXS <= 120) best = s;
+      if (s * W8 * 8 + 2 * MAXS <= 116) best = s;
     return best;
   }
   static constexpr int SB = sb();
   static constexpr int NB = (MAXS + SB - 1) / SB;
 };
 
-template <int W8, typename Release>
+// max over 8 columns of D - b[col] (plain operands: b = ||e||^2/2 of the
+// column's element, from shared memory)
+__device__ __forceinline__ float max8b(const uint32_t (&r)[8], const float *b,
+                                       float m) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) m = fmaxf(m, __uint_as_float(r[j]) - b[j]);
+  return m;
+}
+
+template <int W8, bool kPlain, typename Release>
 __device__ __forceinline__ void epi_tile(
-    uint32_t taddr, int h, int spt, int w, float ax, bool valid,
-    double (&acc)[EpiShape<W8>::MAXS], const Release &release) {
+    uint32_t taddr, int h, int spt, int w, float ax, float ha, bool valid,
+    const float *bsm, double (&acc)[EpiShape<W8>::MAXS],
+    const Release &release) {
   const float ninf = -__int_as_float(0x7f800000);
   const int nsets = (spt - h + 1) >> 1;
   if (nsets <= 0) {
     release();
     return;
   }
-  if constexpr (W8 * 8 + 2 * EpiShape<W8>::MAXS <= 120) {
+  if constexpr (W8 * 8 + 2 * EpiShape<W8>::MAXS <= 116) {
     constexpr int SB = EpiShape<W8>::SB;
     constexpr int NB = EpiShape<W8>::NB;
     const int nbat = (nsets + SB - 1) / SB;
@@ -165,9 +178,14 @@ __device__ __forceinline__ void epi_tile(
         for (int j = 0; j < SB; ++j) {
           if (b * SB + j < nsets) {
             float mx = ninf;
+            const int cb = (h + 2 * (b * SB + j)) * w;  // set's first column
 #pragma unroll
-            for (int g = 0; g < W8; ++g) mx = max8(r[j * W8 + g], mx);
-            const float t = fminf(ax, fmaxf(0.f, -2.f * mx));
+            for (int g = 0; g < W8; ++g)
+              mx = kPlain ? max8b(r[j * W8 + g], bsm + cb + 8 * g, mx)
+                          : max8(r[j * W8 + g], mx);
+            // folded: min_e d = -2 max D;  plain: min_e d = a - 2 max (D - b)
+            const float dm = kPlain ? fmaf(-2.f, mx, ha) : -2.f * mx;
+            const float t = fminf(ax, fmaxf(0.f, dm));
             if (valid) acc[b * SB + j] += (double)t;
           }
         }
@@ -191,9 +209,12 @@ __device__ __forceinline__ void epi_tile(
       if (sb == NS - 1) release();
 #pragma unroll
       for (int g = 0; g < G; ++g)
-        if (sb * G + g < W8) mx = max8(r[g], mx);
+        if (sb * G + g < W8)
+          mx = kPlain ? max8b(r[g], bsm + h * w + 8 * (sb * G + g), mx)
+                      : max8(r[g], mx);
     }
-    const float t = fminf(ax, fmaxf(0.f, -2.f * mx));
+    const float dm = kPlain ? fmaf(-2.f, mx, ha) : -2.f * mx;
+    const float t = fminf(ax, fmaxf(0.f, dm));
     if (valid) acc[0] += (double)t;
   }
 }
@@ -204,11 +225,12 @@ __device__ __forceinline__ void epi_tile(
 // pair tile; buffers are released on the leader's tempty, and at item end
 // the peer's per-set sums travel to the leader through DSMEM (xbuf) so the
 // leader writes one fixed-order partial per (split, set).
-template <int CG, int W8>
+template <int CG, int W8, bool kPlain>
 __device__ __forceinline__ void epilogue_role(const BParams &p, uint32_t tmem,
                                               uint64_t *tfull,
                                               uint64_t *tempty, double *red,
-                                              double *xbuf, uint64_t *xfull,
+                                              double *xbuf, float *bsm,
+                                              uint64_t *xfull,
                                               uint64_t *xempty, int warp,
                                               int lane, int64_t items,
                                               uint32_t rank, int64_t pair,
@@ -230,10 +252,16 @@ __device__ __forceinline__ void epilogue_role(const BParams &p, uint32_t tmem,
     double acc[MAXS];
 #pragma unroll
     for (int u = 0; u < MAXS; ++u) acc[u] = 0.0;
+    if constexpr (kPlain) {  // the set tile's column constants, once per item
+      for (int c = ew * 32 + lane; c < p.ncols; c += kEpiWarps * 32)
+        bsm[c] = p.bs[st * p.ncols + c];
+      asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+    }
     for (int64_t pt = p0; pt < p1; pt += BM * CG) {
       const int64_t pi = pt + BM * rank + row;
       const bool valid = pi < p1;
       const float ax = (valid && !(p.dbg & 8)) ? p.aux[pi] : 0.f;
+      const float ha = (kPlain && valid) ? (float)p.norms[pi] : 0.f;
       if (lane == 0) {
         mbar_wait_sleep(&tfull[buf], (tph >> buf) & 1u);
       }
@@ -249,7 +277,8 @@ __device__ __forceinline__ void epilogue_role(const BParams &p, uint32_t tmem,
       if (p.dbg & 1)  // timing experiment: no TMEM drain / math
         rel();
       else
-        epi_tile<W8>(taddr, h, p.spt, p.w, ax, valid, acc, rel);
+        epi_tile<W8, kPlain>(taddr, h, p.spt, p.w, ax, ha, valid, bsm, acc,
+                             rel);
 #ifdef EXEM_TCB_TRACE_BUILD
       if (tr) TRB(4, etile);
       ++etile;
@@ -400,6 +429,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t *tmem_slot = (uint32_t *)(xempty + 1);
   double *red = (double *)(tmem_slot + 4);         // [4][kMaxSpt]
   double *xbuf = red + 4 * kMaxSpt;                // [kMaxSpt]
+  float *bsm = (float *)(xbuf + kMaxSpt);          // [256] plain: set b
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = CG == 2 ? cluster_rank() : 0u;
@@ -639,8 +669,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     switch (p.w >> 3) {
 #define EXEM_EPI_CASE(W)                                                     \
   case W:                                                                    \
-    epilogue_role<CG, W>(p, tmem, tfull, tempty, red, xbuf, xfull, xempty,   \
-                         warp, lane, items, rank, pair, npairs);             \
+    if (p.plain)                                                             \
+      epilogue_role<CG, W, true>(p, tmem, tfull, tempty, red, xbuf, bsm,     \
+                                 xfull, xempty, warp, lane, items, rank,     \
+                                 pair, npairs);                              \
+    else                                                                     \
+      epilogue_role<CG, W, false>(p, tmem, tfull, tempty, red, xbuf, bsm,    \
+                                  xfull, xempty, warp, lane, items, rank,    \
+                                  pair, npairs);                             \
     break;
       EXEM_EPI_CASE(1) EXEM_EPI_CASE(2) EXEM_EPI_CASE(3) EXEM_EPI_CASE(4)
       EXEM_EPI_CASE(5) EXEM_EPI_CASE(6) EXEM_EPI_CASE(7) EXEM_EPI_CASE(8)
@@ -682,7 +718,7 @@ __global__ void pack_sets_kernel(const float *__restrict__ packed,
                                  int64_t l_pad, int k_max, int d, int spt,
                                  int w, int ncols, int64_t rows,
                                  typename Traits<DT>::S *__restrict__ x,
-                                 int64_t kp) {
+                                 int64_t kp, float *__restrict__ bs) {
   using S = typename Traits<DT>::S;
   const int64_t r = (int64_t)blockIdx.x * blockDim.y + threadIdx.y;
   if (r >= rows) return;
@@ -693,9 +729,11 @@ __global__ void pack_sets_kernel(const float *__restrict__ packed,
   const bool real = s < spt && j < l;
   const int src = real ? (e < card[j] ? e : 0) : 0;
   const int64_t ldp = (int64_t)k_max * l_pad;
+  if (bs != nullptr && threadIdx.x == 0)  // plain: the column's b = ||e||^2/2
+    bs[r] = real ? (float)(0.5 * pnorms[(int64_t)src * l_pad + j]) : 0.f;
   for (int k = threadIdx.x; k < kp; k += blockDim.x) {
     double v = 0.0;
-    if (real) {
+    if (real && (bs == nullptr || k < d)) {
       if (k < d) {
         v = (double)packed[(int64_t)k * ldp + (int64_t)src * l_pad + j];
       } else if (k < d + 3) {
@@ -710,6 +748,29 @@ __global__ void pack_sets_kernel(const float *__restrict__ packed,
       }
     }
     x[r * kp + k] = from_d<S>(v);
+  }
+}
+
+// Plain point rows [v, 0..] (kp = round_up(d, 64)) for unfolded K4-TC.
+template <int DT>
+__global__ void pack_plain_kernel(const float *__restrict__ vt, int64_t ld,
+                                  int64_t n, int d,
+                                  typename Traits<DT>::S *__restrict__ x,
+                                  int64_t kp, int64_t rows) {
+  using S = typename Traits<DT>::S;
+  __shared__ float tile[32][33];
+  const int64_t r0 = (int64_t)blockIdx.x * 32;
+  const int k0 = blockIdx.y * 32;
+  for (int ty = threadIdx.y; ty < 32; ty += blockDim.y) {
+    const int k = k0 + ty;
+    const int64_t r = r0 + threadIdx.x;
+    tile[ty][threadIdx.x] = (k < d && r < n) ? vt[(int64_t)k * ld + r] : 0.f;
+  }
+  __syncthreads();
+  for (int ty = threadIdx.y; ty < 32; ty += blockDim.y) {
+    const int64_t r = r0 + ty;
+    const int k = k0 + threadIdx.x;
+    if (r < rows && k < kp) x[r * kp + k] = from_d<S>((double)tile[threadIdx.x][ty]);
   }
 }
 
@@ -746,34 +807,63 @@ int64_t exem_tc_set_rows(int64_t l, int64_t k_max) {
   return ceil_div(l < 1 ? 1 : l, spt) * nc;
 }
 
+int64_t exem_tc_batch_plain(int64_t d) {
+  // unfolded operands when folding the six constant columns would cost a
+  // whole extra 64-wide K chunk (d = 59..64 mod 64, e.g. d = 256)
+  return round_up(d, kTcKChunk) < exem_tc_kp(d) ? 1 : 0;
+}
+
+int64_t exem_tc_batch_kp(int64_t d) {
+  return exem_tc_batch_plain(d) ? round_up(d, kTcKChunk) : exem_tc_kp(d);
+}
+
+int exem_tc_pack_points_plain(int dtype, const void *vt, int64_t ld,
+                              int64_t n, int64_t d, void *xp, void *stream) {
+  if (dtype != EXEM_BF16 && dtype != EXEM_F16)
+    return fail(EXEM_ERR_ARG, "TC operands are bf16/f16 only");
+  const int64_t kp = round_up(d, kTcKChunk), rows = exem_tc_rows(n);
+  dim3 grid((unsigned)ceil_div(rows, 32), (unsigned)ceil_div(kp, 32));
+  dim3 block(32, 8);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == EXEM_BF16)
+    tcb::pack_plain_kernel<EXEM_BF16><<<grid, block, 0, st>>>(
+        (const float *)vt, ld, n, (int)d, (__nv_bfloat16 *)xp, kp, rows);
+  else
+    tcb::pack_plain_kernel<EXEM_F16><<<grid, block, 0, st>>>(
+        (const float *)vt, ld, n, (int)d, (__half *)xp, kp, rows);
+  EXEM_LAUNCH_CHECK("tc_pack_points_plain");
+  return EXEM_OK;
+}
+
 int exem_tc_pack_sets(int dtype, const void *packed, const double *pnorms,
                       const int32_t *card, int64_t l, int64_t l_pad,
-                      int64_t k_max, int64_t d, void *xs, void *stream) {
+                      int64_t k_max, int64_t d, void *xs, float *bs,
+                      void *stream) {
   if (dtype != EXEM_BF16 && dtype != EXEM_F16)
     return fail(EXEM_ERR_ARG, "TC operands are bf16/f16 only");
   int32_t spt, w, nc;
   if (int rc = exem_tc_set_geometry(k_max, &spt, &w, &nc)) return rc;
   const int64_t rows = exem_tc_set_rows(l, k_max);
-  const int64_t kp = exem_tc_kp(d);
+  const int64_t kp = bs ? round_up(d, kTcKChunk) : exem_tc_kp(d);
   dim3 block(64, 4);
   dim3 grid((unsigned)ceil_div(rows, 4));
   cudaStream_t st = (cudaStream_t)stream;
   if (dtype == EXEM_BF16)
     tcb::pack_sets_kernel<EXEM_BF16><<<grid, block, 0, st>>>(
         (const float *)packed, pnorms, card, l, l_pad, (int)k_max, (int)d, spt,
-        w, nc, rows, (__nv_bfloat16 *)xs, kp);
+        w, nc, rows, (__nv_bfloat16 *)xs, kp, bs);
   else
     tcb::pack_sets_kernel<EXEM_F16><<<grid, block, 0, st>>>(
         (const float *)packed, pnorms, card, l, l_pad, (int)k_max, (int)d, spt,
-        w, nc, rows, (__half *)xs, kp);
+        w, nc, rows, (__half *)xs, kp, bs);
   EXEM_LAUNCH_CHECK("tc_pack_sets");
   return EXEM_OK;
 }
 
 int exem_batch_eval_tc(int dtype, const void *xp, int64_t n, const void *aux,
-                       const void *xs, int64_t l, int64_t k_max, int64_t d,
-                       int64_t split_pts, double *partial, int64_t splits,
-                       void *stream) {
+                       const double *norms, const void *xs, const float *bs,
+                       int64_t l, int64_t k_max, int64_t d, int64_t split_pts,
+                       double *partial, int64_t splits, void *stream) {
   using namespace exem::tcb;
   if (dtype != EXEM_BF16 && dtype != EXEM_F16)
     return fail(EXEM_ERR_ARG, "batch_eval_tc is bf16/f16 only");
@@ -793,7 +883,13 @@ int exem_batch_eval_tc(int dtype, const void *xp, int64_t n, const void *aux,
   BParams prm;
   int32_t spt, w, nc;
   if (int rc = exem_tc_set_geometry(k_max, &spt, &w, &nc)) return rc;
-  const int64_t kp = exem_tc_kp(d);
+  const bool plain = bs != nullptr;
+  if (plain && norms == nullptr)
+    return fail(EXEM_ERR_ARG, "batch_eval_tc: plain operands need norms");
+  const int64_t kp = plain ? round_up(d, kTcKChunk) : exem_tc_kp(d);
+  prm.plain = plain ? 1 : 0;
+  prm.norms = norms;
+  prm.bs = bs;
   prm.n = n;
   prm.l = l;
   prm.split_pts = split_pts;
@@ -802,7 +898,7 @@ int exem_batch_eval_tc(int dtype, const void *xp, int64_t n, const void *aux,
   prm.spt = spt;
   prm.w = w;
   prm.ncols = nc;
-  prm.ksteps = (int)ceil_div(d + kTcConst, 16);
+  prm.ksteps = (int)ceil_div(d + (plain ? 0 : kTcConst), 16);
   prm.kchunks = (int)(kp / KCH);
   // Single-CTA tiles by default.  EXEM_TCB_CG=2 selects CTA pairs
   // (cta_group::2, M = 256, each CTA holding half of the set tile, 9 instead

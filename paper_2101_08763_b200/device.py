@@ -128,6 +128,23 @@ class DeviceGround:
                                N.ptr(self._xp0), self.stream)
         return self._xp0
 
+    def xp_batch(self):
+        """Point operand of K4-TC: the m = 0 folded rows, or plain rows when
+        folding would add a K chunk (exem_tc_batch_plain)."""
+        lib = N.lib()
+        if not lib.tc_batch_plain(self.d):
+            return self.xp0()
+        if getattr(self, "_xpp", None) is None:
+            t = torch()
+            tdt = t.bfloat16 if self.precision.tag == N.BF16 else t.float16
+            self._xpp = t.empty((int(lib.tc_rows(self.n)),
+                                 int(lib.tc_batch_kp(self.d))), dtype=tdt,
+                                device=self.dev)
+            lib.tc_pack_points_plain(self.precision.tag, N.ptr(self.vt),
+                                     self.ld, self.n, self.d,
+                                     N.ptr(self._xpp), self.stream)
+        return self._xpp
+
     def xc_split(self):
         """Split-bf16 binary32 candidate operand (exem_tc_pack_split)."""
         if getattr(self, "_xcs", None) is None:

@@ -186,14 +186,18 @@ class DeviceBatch:
         self.card = t.tensor(np.asarray(cardinalities, dtype=np.int32),
                              device=dev)
         self.xs = None
+        self.bs = None
         if tc_batch_supported(precision, k_max):
             rows = int(lib.tc_set_rows(l, k_max))
             tdt = t.bfloat16 if precision.tag == N.BF16 else t.float16
-            self.xs = t.empty((rows, int(lib.tc_kp(d))), dtype=tdt,
+            self.xs = t.empty((rows, int(lib.tc_batch_kp(d))), dtype=tdt,
                               device=dev)
+            if lib.tc_batch_plain(d):  # unfolded operands (K4-TC)
+                self.bs = t.empty(rows, dtype=t.float32, device=dev)
             lib.tc_pack_sets(precision.tag, N.ptr(self.packed),
                              N.ptr(self.pnorms), N.ptr(self.card), l,
-                             self.l_pad, k_max, d, N.ptr(self.xs), stream)
+                             self.l_pad, k_max, d, N.ptr(self.xs),
+                             N.ptr(self.bs), stream)
 
 
 def batch_partials(dg, batch: DeviceBatch, partial, split_pts: int,
@@ -204,9 +208,10 @@ def batch_partials(dg, batch: DeviceBatch, partial, split_pts: int,
     prec = dg.precision
     pp = partial if isinstance(partial, N.c_void_p) else N.ptr(partial)
     if batch.xs is not None:
-        lib.batch_eval_tc(prec.tag, N.ptr(dg.xp0()), dg.n, N.ptr(dg.aux),
-                          N.ptr(batch.xs), batch.l, batch.k_max, dg.d,
-                          split_pts, pp, splits, dg.stream)
+        lib.batch_eval_tc(prec.tag, N.ptr(dg.xp_batch()), dg.n, N.ptr(dg.aux),
+                          N.ptr(dg.norms), N.ptr(batch.xs), N.ptr(batch.bs),
+                          batch.l, batch.k_max, dg.d, split_pts, pp, splits,
+                          dg.stream)
     else:
         lib.batch_eval(prec.tag, N.ptr(dg.vt), dg.ld, dg.n, dg.d,
                        N.ptr(dg.norms), N.ptr(dg.aux), N.ptr(batch.packed),

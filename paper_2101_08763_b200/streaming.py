@@ -51,7 +51,8 @@ def layout_bytes(rows: int, d: int, precision, with_src: bool = False,
     cs = _csize(precision)
     b = d_pad * ld * cs + ld * 8 + ld * cs
     if precision.is_half:
-        b += tc_operands * int(lib.tc_rows(rows)) * int(lib.tc_kp(d)) * 2
+        kp = max(int(lib.tc_kp(d)), int(lib.tc_batch_kp(d)))
+        b += tc_operands * int(lib.tc_rows(rows)) * kp * 2
     if with_src:
         b += rows * d * precision.bytes_per_value
     return b
@@ -145,10 +146,12 @@ class _Slot:
         self.norms = t.empty(ldc, dtype=t.float64, device=dev)
         self.aux = t.empty(ldc, dtype=cdt, device=dev)
         self.kp = int(lib.tc_kp(d)) if precision.is_half else 0
+        self.plain = bool(precision.is_half and lib.tc_batch_plain(d))
         self._xp = None
         if precision.is_half:
             tdt = t.bfloat16 if precision.tag == N.BF16 else t.float16
-            self._xp = t.empty((int(lib.tc_rows(cap)), self.kp), dtype=tdt,
+            kp = max(self.kp, int(lib.tc_batch_kp(d)))
+            self._xp = t.empty((int(lib.tc_rows(cap)), kp), dtype=tdt,
                                device=dev)
         self.uploaded = t.cuda.Event()
         self.consumed = t.cuda.Event()
@@ -164,6 +167,10 @@ class _Slot:
         return N.stream_handle(self.dev)
 
     def xp0(self):
+        return self._xp
+
+    def xp_batch(self):
+        """K4-TC point operand of the slice (packed by ``slices``)."""
         return self._xp
 
 
@@ -237,9 +244,14 @@ class GroundStream:
                                    self.block_ptr(r0), st)
                 slot.consumed.record(compute)
                 if prec.is_half and pack_points:
-                    lib.tc_pack_points(prec.tag, N.ptr(slot.vt), slot.ld,
-                                       rows, self.d, N.ptr(slot.norms), None,
-                                       N.ptr(slot.xp0()), st)
+                    if slot.plain:
+                        lib.tc_pack_points_plain(prec.tag, N.ptr(slot.vt),
+                                                 slot.ld, rows, self.d,
+                                                 N.ptr(slot.xp_batch()), st)
+                    else:
+                        lib.tc_pack_points(prec.tag, N.ptr(slot.vt), slot.ld,
+                                           rows, self.d, N.ptr(slot.norms),
+                                           None, N.ptr(slot.xp0()), st)
                 yield slot, r0, r1
 
 
@@ -318,7 +330,7 @@ def batch_device_bytes(d: int, k_max: int, l: int, precision,
     b = int(lib.pad_dims(d)) * k_max * l_pad * _csize(precision)
     b += k_max * l_pad * 8 + 4 * l + splits * l * 8 + 8 * l
     if precision.is_half and k_max <= 256:
-        b += int(lib.tc_set_rows(l, k_max)) * int(lib.tc_kp(d)) * 2
+        b += int(lib.tc_set_rows(l, k_max)) * (int(lib.tc_batch_kp(d)) * 2 + 4)
     return b
 
 
