@@ -106,6 +106,7 @@ __global__ void __launch_bounds__(kRedThreads)
 // in chunks of kSetChunk rows and each thread keeps kSetChunk dot products in
 // registers, so V is streamed ceil(k / kSetChunk) times (HBM-bound).
 constexpr int kSetChunk = 8;
+constexpr int kLoadAhead = 8;  // independent V loads in flight per thread
 
 template <int DT>
 __global__ void __launch_bounds__(kRedThreads)
@@ -136,7 +137,27 @@ __global__ void __launch_bounds__(kRedThreads)
 #pragma unroll
     for (int e = 0; e < kSetChunk; ++e) acc[e] = C(0);
     if (live) {
-      for (int kk = 0; kk < d; ++kk) {
+      // HBM-bound: issue kLoadAhead independent coalesced loads per thread
+      // before using them (memory-level parallelism), then the FMAs
+      int kk = 0;
+      for (; kk + kLoadAhead <= d; kk += kLoadAhead) {
+        C xs[kLoadAhead];
+#pragma unroll
+        for (int u = 0; u < kLoadAhead; ++u)
+          xs[u] = vt[(int64_t)(kk + u) * ld + i];
+#pragma unroll
+        for (int u = 0; u < kLoadAhead; ++u)
+#pragma unroll
+          for (int e = 0; e < kSetChunk; ++e) {
+            if (Traits<DT>::kDirect) {
+              const C df = xs[u] - se[e * d_pad + kk + u];
+              acc[e] = fma(df, df, acc[e]);
+            } else {
+              acc[e] = fma(xs[u], se[e * d_pad + kk + u], acc[e]);
+            }
+          }
+      }
+      for (; kk < d; ++kk) {
         const C x = vt[(int64_t)kk * ld + i];
 #pragma unroll
         for (int e = 0; e < kSetChunk; ++e) {
@@ -248,7 +269,24 @@ __global__ void __launch_bounds__(kRedThreads)
   double v = 0.0;
   if (i < n) {
     C acc = C(0);
-    for (int kk = 0; kk < d; ++kk) {
+    int kk = 0;
+    for (; kk + kLoadAhead <= d; kk += kLoadAhead) {  // loads ahead (MLP)
+      C xs[kLoadAhead];
+#pragma unroll
+      for (int u = 0; u < kLoadAhead; ++u)
+        xs[u] = vt[(int64_t)(kk + u) * ld + i];
+#pragma unroll
+      for (int u = 0; u < kLoadAhead; ++u) {
+        const C y = cvt[(int64_t)(kk + u) * ldc + c];
+        if (Traits<DT>::kDirect) {
+          const C df = xs[u] - y;
+          acc = fma(df, df, acc);
+        } else {
+          acc = fma(xs[u], y, acc);
+        }
+      }
+    }
+    for (; kk < d; ++kk) {
       const C x = vt[(int64_t)kk * ld + i];
       const C y = cvt[(int64_t)kk * ldc + c];
       if (Traits<DT>::kDirect) {

@@ -1,0 +1,112 @@
+"""HBM-roofline evidence for the memory-bound kernels:
+K1 ground_prepare, K2 set_min (single-set evaluate, k = 1/10/50) and the
+Greedy m-update (greedy_update), timed with CUDA events at n = 1M, d = 100,
+fp32 (and bf16 storage for K1).  Algorithmic bytes per launch:
+
+  K1            read n*d*b (storage) + write n*d_pad*4 (vt) + 16n (norms, aux)
+  set_min       ceil(k/8) passes over vt (n*d_pad*4 each) + 8n norms + 4n aux
+                (+ 4n t_out when requested)
+  greedy_update read vt (n*d_pad*4) + 8n norms + 4n m, write 4n m
+
+achieved = bytes / median launch time; peak = MEASURED_PEAKS.json hbm_gbs.
+
+    python tools/hbm_kernels.py [--n 1000000] [--d 100]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+
+def timed(fn, reps=5):
+    import torch
+
+    fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b) / 1e3)
+    return float(np.median(ts))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=int, default=1_000_000)
+    ap.add_argument("--d", type=int, default=100)
+    args = ap.parse_args()
+    import torch
+
+    import paper_2101_08763_b200 as pb
+    from paper_2101_08763_b200 import _native as N
+    from paper_2101_08763_b200.device import padded_rows, to_device_bytes
+
+    torch.cuda.set_device(0)
+    lib = N.lib()
+    peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] \
+        if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0
+    n, d = args.n, args.d
+    V = np.random.default_rng(0).standard_normal((n, d), dtype=np.float32)
+    out = []
+
+    def rec(name, bytes_, t):
+        r = {"kernel": name, "n": n, "d": d, "bytes": bytes_, "ms": t * 1e3,
+             "achieved_gbs": bytes_ / t / 1e9, "peak_gbs": peak,
+             "frac": bytes_ / t / 1e9 / peak}
+        out.append(r)
+        print(json.dumps(r), flush=True)
+
+    for prec in (pb.Precision.binary32, pb.Precision.bfloat16):
+        g = pb.build_ground_set(V, precision=prec)
+        dg = g.on_device()
+        st = N.stream_handle()
+        src = to_device_bytes(g.matrix.ravel(order="F"), dg.dev)
+        e0 = to_device_bytes(g.aux, dg.dev)
+        t = timed(lambda: lib.ground_prepare(
+            prec.tag, N.ptr(src), n, d, N.ptr(e0), N.ptr(dg.vt), dg.ld,
+            N.ptr(dg.norms), N.ptr(dg.aux), N.ptr(dg.aux_sum),
+            N.ptr(dg.scratch), st))
+        rec(f"K1 ground_prepare ({prec.value})",
+            n * d * prec.bytes_per_value + n * dg.d_pad * 4 + 16 * n, t)
+        if prec is not pb.Precision.binary32:
+            continue
+        for k in (1, 10, 50):
+            elems = padded_rows(g.matrix[:k], dg.d_pad, prec, dg.dev)
+            en = torch.empty(k, dtype=torch.float64, device=dg.dev)
+            lib.row_norms(prec.tag, N.ptr(elems), k, d, dg.d_pad, N.ptr(en), st)
+            s = torch.empty(1, dtype=torch.float64, device=dg.dev)
+            t = timed(lambda: lib.set_min(
+                prec.tag, N.ptr(dg.vt), dg.ld, n, d, N.ptr(dg.norms),
+                N.ptr(dg.aux), N.ptr(elems), N.ptr(en), k, 1, None, None,
+                N.ptr(s), N.ptr(dg.scratch), st))
+            rec(f"K2 set_min k={k} (single-set evaluate)",
+                -(-k // 8) * n * dg.d_pad * 4 + 12 * n, t)
+        m = torch.empty(dg.ld, dtype=torch.float32, device=dg.dev)
+        m.copy_(dg.aux)
+        sel = torch.zeros(1, dtype=torch.int64, device=dg.dev)
+        msum = torch.empty(1, dtype=torch.float64, device=dg.dev)
+        t = timed(lambda: lib.greedy_update(
+            prec.tag, N.ptr(dg.vt), dg.ld, n, d, N.ptr(dg.norms),
+            N.ptr(dg.vt), dg.ld, N.ptr(dg.norms), N.ptr(sel), 0, N.ptr(m),
+            None, 0, N.ptr(msum), N.ptr(dg.scratch), st))
+        rec("K2 greedy_update (m-update)", n * dg.d_pad * 4 + 20 * n, t)
+    (ROOT / "gpurun_out").mkdir(exist_ok=True)
+    (ROOT / "gpurun_out" / "hbm_kernels.jsonl").write_text(
+        "".join(json.dumps(r) + "\n" for r in out))
+
+
+if __name__ == "__main__":
+    main()
