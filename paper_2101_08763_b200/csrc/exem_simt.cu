@@ -326,10 +326,12 @@ __global__ void __launch_bounds__(kRedThreads)
 // (r<4 ? ty*4+r : 64+ty*4+r-4); same for columns with tx.
 constexpr int kBM = 128, kBN = 128, kBK = 8, kThreads = 256;
 
+constexpr int kSimtStages = 3;  // cp.async ring: one barrier per k-chunk
+
 template <typename T>
 struct SimtSmem {
-  T a[2][kBK][kBM];
-  T b[2][kBK][kBN];
+  T a[kSimtStages][kBK][kBM];
+  T b[kSimtStages][kBK][kBN];
 };
 
 template <typename T>
@@ -380,23 +382,32 @@ __device__ __forceinline__ void simt_mainloop(SimtSmem<T> &sm, const T *arow,
                                               const T *bpts, int64_t ldb,
                                               int64_t b0, int d_pad, int tx,
                                               int ty, T (&acc)[8][8]) {
+  // Three-buffer cp.async ring: chunk c lives in buffer c % 3 and cp.async
+  // group c.  Each iteration waits for its chunk, then ONE barrier both
+  // publishes it and proves every thread has finished chunk c-1, whose
+  // buffer the load of chunk c+2 then overwrites.
   const int nk = d_pad / kBK;
-  __syncthreads();  // previous consumers of both buffers are done
+  __syncthreads();  // previous consumers of the ring are done
   load_chunk<T>(sm.a[0], arow, lda, a0, 0);
   load_chunk<T>(sm.b[0], bpts, ldb, b0, 0);
   cp_async_commit();
+  if (nk > 1) {
+    load_chunk<T>(sm.a[1], arow, lda, a0, kBK);
+    load_chunk<T>(sm.b[1], bpts, ldb, b0, kBK);
+  }
+  cp_async_commit();
+  int buf = 0;
   for (int c = 0; c < nk; ++c) {
-    if (c + 1 < nk) {
-      load_chunk<T>(sm.a[(c + 1) & 1], arow, lda, a0, (c + 1) * kBK);
-      load_chunk<T>(sm.b[(c + 1) & 1], bpts, ldb, b0, (c + 1) * kBK);
-      cp_async_commit();
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
+    cp_async_wait<1>();
+    __syncthreads();
+    if (c + 2 < nk) {
+      const int nb = buf == 0 ? 2 : buf - 1;  // (c + 2) % 3
+      load_chunk<T>(sm.a[nb], arow, lda, a0, (c + 2) * kBK);
+      load_chunk<T>(sm.b[nb], bpts, ldb, b0, (c + 2) * kBK);
     }
-    __syncthreads();
-    mma_chunk<T, kDirect>(sm, c & 1, tx, ty, acc);
-    __syncthreads();
+    cp_async_commit();  // (possibly empty: keeps group c+2 = chunk c+2)
+    mma_chunk<T, kDirect>(sm, buf, tx, ty, acc);
+    buf = buf == 2 ? 0 : buf + 1;
   }
 }
 
@@ -951,7 +962,12 @@ int exem_greedy_gains_simt(int dtype, const void *cvt, int64_t ldc,
         (const float *)m, n, d_pad, split_pts, partial);
     EXEM_LAUNCH_CHECK("gains_simt_kernel<f32>");
   } else if (dtype == EXEM_F64) {
-    size_t smem = sizeof(SimtSmem<double>);
+    size_t smem = sizeof(SimtSmem<double>);  // 48 KB: needs the opt-in
+    cudaError_t e = cudaFuncSetAttribute(
+        gains_simt_kernel<double, 1>,
+        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess)
+      return fail(EXEM_ERR_CUDA, "gains_simt smem: %s", cudaGetErrorString(e));
     gains_simt_kernel<double, 1><<<grid, kThreads, smem, st>>>(
         (const double *)cvt, ldc, cnorms, l, (const double *)vt, ld, norms,
         (const double *)m, n, d_pad, split_pts, partial);
