@@ -1,0 +1,77 @@
+"""The product's multi-rank entry points run for real: two processes over
+torch.distributed (gloo -- the one-GPU test box cannot host two NCCL ranks),
+both on cuda:0, each owning a row shard of V.
+
+* sharded_batch_sums (BASELINE config 5's path): per-set sums identical BIT
+  FOR BIT to the single-process evaluate_batch (exact zero-padded partial
+  all-reduce + fixed-order reduction).
+* sharded_greedy (config 4's path): the same picks as the single-process
+  Greedy, values within fp64 summation-order rounding.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, V, sets, k, out):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2101_08763_b200 as pb
+    from paper_2101_08763_b200.distributed import (build_sharded_ground,
+                                                   sharded_batch_sums,
+                                                   sharded_greedy)
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        prec = pb.Precision.bfloat16
+        g = pb.build_ground_set(V, precision=prec)
+        batch = pb.EvaluationBatch.from_sets([g.matrix[i] for i in sets])
+        sums = sharded_batch_sums(g, batch, rank, world)
+        sg = build_sharded_ground(V, prec, rank, world, device=0)
+        picks, vals = sharded_greedy(sg, k)
+        out[rank] = (sums.cpu().numpy(), list(picks), list(vals))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_ranks_match_single_process():
+    import paper_2101_08763_b200 as pb
+    from paper_2101_08763_b200 import Evaluator
+
+    rng = np.random.default_rng(21)
+    n, d, k = 70_000, 24, 3
+    V = rng.standard_normal((n, d)).astype(np.float32)
+    sets = [np.sort(rng.choice(n, size=int(rng.integers(1, 20)), replace=False))
+            for _ in range(30)]
+    g = pb.build_ground_set(V, precision=pb.Precision.bfloat16)
+    batch = pb.EvaluationBatch.from_sets([g.matrix[i] for i in sets])
+    ref_vals = pb.evaluate_batch(Evaluator(), g, batch)
+    ref_greedy = pb.greedy_maximize(g, k=k)
+    ctx = mp.get_context("spawn")
+    mgr = ctx.Manager()
+    out = mgr.dict()
+    mp.start_processes(_worker, args=(2, _free_port(), V, sets, k, out),
+                       nprocs=2, join=True, start_method="spawn")
+    acc = g.precision.accumulate_dtype
+    for rank in range(2):
+        sums, picks, vals = out[rank]
+        got = acc.type(g.aux_loss) - sums.astype(acc) / acc.type(n)
+        assert np.array_equal(got, ref_vals), rank
+        assert picks == list(ref_greedy.exemplar_indices)
+        assert np.allclose(vals, ref_greedy.values, rtol=1e-6, atol=1e-6)
