@@ -250,20 +250,37 @@ def main():
     ev = []
     orig = run.compute_gains
 
-    def timed_gains(chunk=None):
+    def timed_gains(chunk=None, out=None):
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        orig(chunk)
+        orig(chunk, out=out)
         b.record(stream)
         ev.append((a, b))
 
+    # EXEM_PEER_REDUCE=1 (N > 1): per-step exchange over CUDA-IPC peer memory
+    # (distributed.PeerGains: fixed-order sum fused into the argmax) instead
+    # of the NCCL all-reduce
+    peer = None
+    if world > 1 and os.environ.get("EXEM_PEER_REDUCE") == "1":
+        from paper_2101_08763_b200.distributed import PeerGains
+
+        peer = PeerGains(run.l, run.dg.dev)
+
+    def do_step(step):
+        if peer is None:
+            ops.local_gains()
+            all_reduce(ops.gains_buffer())
+            ops.select(step)
+        else:
+            run.compute_gains(out=peer.local_buffer(step))
+            peer.publish(step, run.stream)
+            peer.select(run, step)
+        ops.update(step)
+
     ops.start()
     for step in range(args.warmup):
-        ops.local_gains()
-        all_reduce(ops.gains_buffer())
-        ops.select(step)
-        ops.update(step)
+        do_step(step)
     torch.cuda.synchronize()
     barrier()
     run.compute_gains = timed_gains
@@ -275,16 +292,15 @@ def main():
         barrier()
         t0.record(stream)
         for step in range(args.warmup, k):
-            ops.local_gains()
-            all_reduce(ops.gains_buffer())
-            ops.select(step)
-            ops.update(step)
+            do_step(step)
         t1.record(stream)
         torch.cuda.synchronize()
         barrier()
     launches = lib.launch_count() - launches0
     ms_local = t0.elapsed_time(t1)
     run.compute_gains = orig
+    if peer is not None:
+        peer.close()
     all_reduce(ops.msum_buffer())
     ms_t = torch.tensor([ms_local], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -349,6 +365,9 @@ def main():
             "vs_baseline": None, "dtype": args.precision,
             "data": f"synthetic Gaussian N(0,1) float32 seed {args.seed}, "
                     f"stored as {args.precision}",
+            "exchange": "peer memory (CUDA IPC, fused sum+argmax)" if peer
+            is not None else (f"{dist.get_backend()} all-reduce" if world > 1
+                              else "none"),
             "config": {"workload": "C4 full Greedy k=50: one step = all l=n-t "
                        "candidate sets S u {c} (K3 gains + K6 + K5 argmax + "
                        "K2 m-update)" + (" [fp32 gains on tensor cores, "

@@ -322,6 +322,33 @@ int exem_sieve_gains(int dtype, const void *M, int64_t ldm, int64_t sieves,
 int exem_sieve_update(int dtype, void *m, const void *dist, int64_t n,
                       double *msum, double *scratch, void *stream);
 
+/*
+ * Multi-GPU K5 over peer memory (no NCCL on the per-step path; distributed.py
+ * PeerGains).  Shared buffers are allocated here (their base pointers are
+ * what CUDA IPC exports) and owned by the caller:
+ *   exem_ipc_alloc / exem_ipc_free      cudaMalloc / cudaFree
+ *   exem_ipc_handle / exem_ipc_open / exem_ipc_close  64-byte CUDA IPC handle
+ *   exem_peer_publish   after this rank's K3 + K6: flag = value (release,
+ *                       system scope; stream-ordered after the gains)
+ *   exem_peer_argmax_select  waits until every peer's flag >= expect, sums
+ *       the W peers' local gains in fixed rank order (x scale) into
+ *       gains_out and takes the masked argmax (as exem_argmax_select).
+ *   peers / flags: device arrays of W device pointers (peer-mapped).
+ */
+int exem_ipc_alloc(int64_t bytes, void **ptr);
+int exem_ipc_free(void *ptr);
+int exem_ipc_handle(void *ptr, void *handle);
+int exem_ipc_open(const void *handle, void **ptr);
+int exem_ipc_close(void *ptr);
+int exem_peer_publish(unsigned long long *flag, unsigned long long value,
+                      void *stream);
+int exem_peer_argmax_select(const double *const *peers,
+                            const unsigned long long *const *flags, int world,
+                            unsigned long long expect, int64_t l, double scale,
+                            double *gains_out, uint8_t *selected,
+                            int64_t step, int64_t *sel_idx, double *sel_gain,
+                            double *scratch, void *stream);
+
 /* Number of kernels this library launched since load (evidence counter). */
 int64_t exem_launch_count(void);
 

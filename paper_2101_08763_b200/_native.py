@@ -93,6 +93,15 @@ _SIGNATURES = {
     "exem_sieve_gains": (c_int, [c_int, _P, c_int64, c_int64, _P, c_int64,
                                  _P, _P, _P]),
     "exem_sieve_update": (c_int, [c_int, _P, _P, c_int64, _P, _P, _P]),
+    "exem_ipc_alloc": (c_int, [c_int64, _P]),
+    "exem_ipc_free": (c_int, [_P]),
+    "exem_ipc_handle": (c_int, [_P, _P]),
+    "exem_ipc_open": (c_int, [_P, _P]),
+    "exem_ipc_close": (c_int, [_P]),
+    "exem_peer_publish": (c_int, [_P, ctypes.c_uint64, _P]),
+    "exem_peer_argmax_select": (c_int, [_P, _P, c_int, ctypes.c_uint64,
+                                        c_int64, c_double, _P, _P, c_int64,
+                                        _P, _P, _P, _P]),
     "exem_launch_count": (c_int64, []),
 }
 

@@ -15,6 +15,8 @@
 // reference's fixed COL_BLOCK sweep (core.py:27-30).
 #include <cfloat>
 
+#include <cstring>
+
 #include "exem_common.cuh"
 
 namespace exem {
@@ -667,6 +669,59 @@ __global__ void __launch_bounds__(kArgThreads)
   }
 }
 
+// ============================================================ peer reduce
+// Multi-GPU K5 without NCCL: every rank's local gains vector lives in an
+// IPC-shared buffer; after its K3 + K6 a rank publishes a step counter
+// (release, system scope).  The consumer kernel on every rank waits for all
+// peers' counters (acquire), sums the W local vectors in fixed rank order
+// straight out of peer memory over NVLink and runs the argmax partial in the
+// same pass -- the collective fused into its consumer, and the summation
+// order (hence the picks) independent of the rank's position and of any
+// NCCL algorithm choice.
+__global__ void peer_publish_kernel(unsigned long long *flag,
+                                    unsigned long long value) {
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(value)
+               : "memory");
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(
+    const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p)
+               : "memory");
+  return v;
+}
+
+__global__ void __launch_bounds__(kArgThreads)
+    peer_argmax_partial_kernel(const double *const *__restrict__ peers,
+                               const unsigned long long *const *__restrict__ flags,
+                               int world, unsigned long long expect,
+                               int64_t l, double scale,
+                               double *__restrict__ gains_out,
+                               const uint8_t *__restrict__ selected,
+                               double *__restrict__ scratch) {
+  if (threadIdx.x < world) {
+    const unsigned long long *f = flags[threadIdx.x];
+    while (ld_acquire_sys(f) < expect) __nanosleep(100);
+  }
+  __syncthreads();
+  Best x{-tinf<double>(), INT64_MAX};
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < l;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    double v = 0.0;
+    for (int r = 0; r < world; ++r) v += peers[r][j];  // fixed rank order
+    v *= scale;
+    gains_out[j] = v;
+    if (!selected[j] && !(v != v)) x = better(x, Best{v, j});
+  }
+  x = block_best(x);
+  if (threadIdx.x == 0) {
+    scratch[2 * blockIdx.x] = x.v;
+    scratch[2 * blockIdx.x + 1] = __longlong_as_double((long long)x.i);
+  }
+}
+
 // ============================================================ distances
 template <int DT>
 __global__ void distance_matrix_kernel(const typename Traits<DT>::C *a,
@@ -1135,6 +1190,76 @@ int exem_sieve_update(int dtype, void *m, const void *dist, int64_t n,
         (float *)m, (const float *)dist, n, scratch);
   EXEM_LAUNCH_CHECK("sieve_update_kernel");
   return reduce_fixed(scratch, blocks, msum, 0, st);
+}
+
+int exem_ipc_alloc(int64_t bytes, void **ptr) {
+  if (bytes < 1) return fail(EXEM_ERR_ARG, "ipc_alloc: bytes must be >= 1");
+  cudaError_t e = cudaMalloc(ptr, (size_t)bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(EXEM_ERR_OOM, "ipc_alloc: %s", cudaGetErrorString(e));
+  }
+  return EXEM_OK;
+}
+
+int exem_ipc_free(void *ptr) {
+  cudaError_t e = cudaFree(ptr);
+  if (e != cudaSuccess)
+    return fail(EXEM_ERR_CUDA, "ipc_free: %s", cudaGetErrorString(e));
+  return EXEM_OK;
+}
+
+int exem_ipc_handle(void *ptr, void *handle) {
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, ptr);
+  if (e != cudaSuccess)
+    return fail(EXEM_ERR_CUDA, "cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
+  memcpy(handle, &h, sizeof(h));
+  return EXEM_OK;
+}
+
+int exem_ipc_open(const void *handle, void **ptr) {
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  cudaError_t e = cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess)
+    return fail(EXEM_ERR_CUDA, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+  return EXEM_OK;
+}
+
+int exem_ipc_close(void *ptr) {
+  cudaError_t e = cudaIpcCloseMemHandle(ptr);
+  if (e != cudaSuccess)
+    return fail(EXEM_ERR_CUDA, "cudaIpcCloseMemHandle: %s", cudaGetErrorString(e));
+  return EXEM_OK;
+}
+
+int exem_peer_publish(unsigned long long *flag, unsigned long long value,
+                      void *stream) {
+  peer_publish_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(flag, value);
+  EXEM_LAUNCH_CHECK("peer_publish_kernel");
+  return EXEM_OK;
+}
+
+int exem_peer_argmax_select(const double *const *peers,
+                            const unsigned long long *const *flags, int world,
+                            unsigned long long expect, int64_t l, double scale,
+                            double *gains_out, uint8_t *selected,
+                            int64_t step, int64_t *sel_idx, double *sel_gain,
+                            double *scratch, void *stream) {
+  if (l < 1 || world < 1 || world > kArgThreads)
+    return fail(EXEM_ERR_ARG, "peer_argmax_select: bad shape");
+  cudaStream_t st = (cudaStream_t)stream;
+  int nb = (int)ceil_div(l, kArgThreads);
+  if (nb > 296) nb = 296;
+  peer_argmax_partial_kernel<<<nb, kArgThreads, 0, st>>>(
+      peers, flags, world, expect, l, scale, gains_out, selected, scratch);
+  EXEM_LAUNCH_CHECK("peer_argmax_partial_kernel");
+  argmax_final_kernel<<<1, kArgThreads, 0, st>>>(scratch, nb, selected,
+                                                 nullptr, step, sel_idx,
+                                                 sel_gain);
+  EXEM_LAUNCH_CHECK("argmax_final_kernel");
+  return EXEM_OK;
 }
 
 }  // extern "C"

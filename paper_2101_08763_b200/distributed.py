@@ -198,3 +198,132 @@ def sharded_batch_sums(ground, batch, rank: int, world: int, group=None,
     lib.reduce_partials(N.ptr(partial), splits, batch.l, 1.0, N.ptr(sums),
                         N.stream_handle(dev))
     return sums
+
+
+# ------------------------------------------------------- peer-memory K5
+class PeerGains:
+    """Per-step gains exchange over peer memory instead of an NCCL
+    all-reduce (opt-in; ``peer_greedy``).
+
+    Every rank owns an IPC-shared buffer holding its local gains for two
+    step parities plus a step flag.  After its K3 + K6 a rank publishes
+    ``flag = step + 1``; ``select`` then runs exem_peer_argmax_select, which
+    waits for all flags, sums the W local vectors in fixed rank order
+    directly from the peers' memory (NVLink P2P on a B200 node) and takes the
+    argmax -- identical on every rank, and independent of any collective
+    algorithm.  Step t writes parity t % 2; a rank can only reach step t+2
+    after every peer published step t+1, which each peer does after its
+    step-t read, so a buffer is never overwritten while being read.
+    """
+
+    def __init__(self, l: int, device, group=None):
+        import ctypes
+
+        import torch
+        import torch.distributed as dist
+
+        from . import _native as N
+
+        self.lib = lib = N.lib()
+        self.l = l
+        self.dev = device
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.group = group
+        ptr = ctypes.c_void_p()
+        lib.ipc_alloc(2 * l * 8, ctypes.byref(ptr))
+        self.own = ptr.value
+        fptr = ctypes.c_void_p()
+        lib.ipc_alloc(8, ctypes.byref(fptr))
+        self.own_flag = fptr.value
+        st = N.stream_handle(device)
+        lib.peer_publish(N.c_void_p(self.own_flag), 0, st)
+        torch.cuda.synchronize(device)
+        handles = []
+        for p_ in (self.own, self.own_flag):
+            h = ctypes.create_string_buffer(64)
+            lib.ipc_handle(N.c_void_p(p_), h)
+            handles.append(h.raw)
+        everyone = [None] * self.world
+        dist.all_gather_object(everyone, handles, group=group)
+        self.opened = []
+        gains_ptrs, flag_ptrs = [], []
+        for q, (gh, fh) in enumerate(everyone):
+            if q == self.rank:
+                gains_ptrs.append(self.own)
+                flag_ptrs.append(self.own_flag)
+                continue
+            for h, dst in ((gh, gains_ptrs), (fh, flag_ptrs)):
+                out = ctypes.c_void_p()
+                lib.ipc_open(ctypes.create_string_buffer(h, 64), ctypes.byref(out))
+                self.opened.append(out.value)
+                dst.append(out.value)
+        self.peers = torch.tensor(
+            [[p_ + par * l * 8 for p_ in gains_ptrs] for par in (0, 1)],
+            dtype=torch.int64, device=device)
+        self.flags = torch.tensor(flag_ptrs, dtype=torch.int64, device=device)
+
+    def local_buffer(self, step: int):
+        from . import _native as N
+
+        return N.c_void_p(self.own + (step % 2) * self.l * 8)
+
+    def publish(self, step: int, stream) -> None:
+        from . import _native as N
+
+        self.lib.peer_publish(N.c_void_p(self.own_flag), step + 1, stream)
+
+    def select(self, run, step: int) -> None:
+        """Fixed-order sum of the peers' gains + masked argmax (K5)."""
+        from . import _native as N
+
+        self.lib.peer_argmax_select(
+            N.c_void_p(self.peers[step % 2].data_ptr()),
+            N.c_void_p(self.flags.data_ptr()), self.world, step + 1, self.l,
+            1.0, N.ptr(run.gains), N.ptr(run.selected), step,
+            N.ptr(run.sel_idx), N.ptr(run.sel_gain), N.ptr(run.scratch),
+            run.stream)
+
+    def close(self) -> None:
+        import torch
+        import torch.distributed as dist
+
+        from . import _native as N
+
+        torch.cuda.synchronize(self.dev)
+        dist.barrier(group=self.group)  # no peer reads our buffers any more
+        for p_ in self.opened:
+            self.lib.ipc_close(N.c_void_p(p_))
+        dist.barrier(group=self.group)
+        self.lib.ipc_free(N.c_void_p(self.own))
+        self.lib.ipc_free(N.c_void_p(self.own_flag))
+
+
+def peer_greedy(sg: ShardedGround, k: int, group=None):
+    """Row-sharded Greedy with the per-step exchange over peer memory
+    (PeerGains) instead of NCCL; one host all-reduce of the k trajectory
+    sums at the end.  Returns (picks, values) like ``sharded_greedy``."""
+    import torch.distributed as dist
+
+    from . import _native as N
+    from .optimize import GreedyRun
+
+    sp = int(N.lib().split_points(sg.n))
+    run = GreedyRun(sg.local, cand=sg.cand, k_cap=k, split_pts=sp)
+    peer = PeerGains(run.l, run.dg.dev, group)
+    try:
+        run.start()
+        for step in range(k):
+            run.compute_gains(out=peer.local_buffer(step))
+            peer.publish(step, run.stream)
+            peer.select(run, step)
+            run.update(step)
+        if dist.is_initialized():
+            dist.all_reduce(run.msum, op=dist.ReduceOp.SUM, group=group)
+        picks = run.sel_idx.cpu().numpy()[:k]
+        msum = run.msum.cpu().numpy()[:k]
+    finally:
+        peer.close()
+    acc = sg.precision.accumulate_dtype
+    vals = acc.type(sg.aux_loss) - msum.astype(acc) / acc.type(sg.n)
+    return tuple(int(i) for i in picks), tuple(float(v) for v in vals)

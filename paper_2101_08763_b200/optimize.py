@@ -145,8 +145,9 @@ class GreedyRun:
                                N.ptr(dg.norms), N.ptr(self.m), N.ptr(self.xp),
                                self.stream)
 
-    def compute_gains(self, chunk: Optional[int] = None):
-        """K3 + K6: gains[c] = sum_{local i} max(0, m_i - d(v_i, c))."""
+    def compute_gains(self, chunk: Optional[int] = None, out=None):
+        """K3 + K6: gains[c] = sum_{local i} max(0, m_i - d(v_i, c)), into
+        ``self.gains`` or the device buffer at pointer ``out``."""
         dg, cd, lib, st = self.dg, self.cand, self.lib, self.stream
         chunk = self.l if not chunk or chunk >= self.l else chunk
         esz = dg.vt.element_size()
@@ -167,8 +168,9 @@ class GreedyRun:
                                       N.ptr(self.m), dg.n, dg.d,
                                       self.split_pts, N.ptr(part),
                                       self.splits, st)
-            out = N.c_void_p(self.gains.data_ptr() + c0 * 8)
-            lib.reduce_partials(N.ptr(part), self.splits, cl, 2.0, out, st)
+            base = self.gains.data_ptr() if out is None else out.value
+            lib.reduce_partials(N.ptr(part), self.splits, cl, 2.0,
+                                N.c_void_p(base + c0 * 8), st)
 
     def select(self, step: int):
         """K5: masked argmax (lowest index on ties) -> sel_idx[step]."""

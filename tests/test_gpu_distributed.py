@@ -7,6 +7,9 @@ both on cuda:0, each owning a row shard of V.
   all-reduce + fixed-order reduction).
 * sharded_greedy (config 4's path): the same picks as the single-process
   Greedy, values within fp64 summation-order rounding.
+* peer_greedy: the per-step exchange over CUDA-IPC peer memory (flag
+  release/acquire + fixed-order sum fused into the argmax) instead of a
+  collective -- same picks, identical results on both ranks.
 """
 
 import os
@@ -31,6 +34,7 @@ def _worker(rank, world, port, V, sets, k, out):
 
     import paper_2101_08763_b200 as pb
     from paper_2101_08763_b200.distributed import (build_sharded_ground,
+                                                   peer_greedy,
                                                    sharded_batch_sums,
                                                    sharded_greedy)
 
@@ -45,7 +49,9 @@ def _worker(rank, world, port, V, sets, k, out):
         sums = sharded_batch_sums(g, batch, rank, world)
         sg = build_sharded_ground(V, prec, rank, world, device=0)
         picks, vals = sharded_greedy(sg, k)
-        out[rank] = (sums.cpu().numpy(), list(picks), list(vals))
+        ppicks, pvals = peer_greedy(sg, k)
+        out[rank] = (sums.cpu().numpy(), list(picks), list(vals),
+                     list(ppicks), list(pvals))
     finally:
         dist.destroy_process_group()
 
@@ -70,8 +76,12 @@ def test_two_ranks_match_single_process():
                        nprocs=2, join=True, start_method="spawn")
     acc = g.precision.accumulate_dtype
     for rank in range(2):
-        sums, picks, vals = out[rank]
+        sums, picks, vals, ppicks, pvals = out[rank]
         got = acc.type(g.aux_loss) - sums.astype(acc) / acc.type(n)
         assert np.array_equal(got, ref_vals), rank
         assert picks == list(ref_greedy.exemplar_indices)
         assert np.allclose(vals, ref_greedy.values, rtol=1e-6, atol=1e-6)
+        # the peer-memory exchange (fixed rank order, no collective per step)
+        assert ppicks == picks
+        assert np.allclose(pvals, vals, rtol=1e-12, atol=1e-12)
+    assert out[0][3] == out[1][3] and out[0][4] == out[1][4]
