@@ -122,6 +122,39 @@ def greedy_case(n, d, prec_name, picks, seed, pk, split32=False):
     return rec
 
 
+def c1_case():
+    """BASELINE config 1 on the device: single-set f(S) with |S| = 10 and the
+    whole Greedy k = 10, n = 10,000, d = 100, fp32, Gaussian seed 1234
+    (the reference's CPU path: 4.1-4.6 ms per f(S), 294 s for the Greedy
+    on 1 thread, 63 s on 8).  Wall clock of the public
+    calls, host arrays in and out."""
+    import torch
+
+    import paper_2101_08763_b200 as pb
+
+    rng = np.random.default_rng(1234)
+    V = rng.standard_normal((10000, 100), dtype=np.float32)
+    S = np.sort(rng.choice(10000, size=10, replace=False))
+    g = pb.build_ground_set(V, precision=pb.Precision.binary32)
+    pb.evaluate_single(g, g.matrix[S])
+    torch.cuda.synchronize()
+    reps = 50
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        pb.evaluate_single(g, g.matrix[S])
+    t_single = (time.perf_counter() - t0) / reps
+    pb.greedy_maximize(g, k=10)
+    t0 = time.perf_counter()
+    res = pb.greedy_maximize(g, k=10)
+    t_greedy = time.perf_counter() - t0
+    return {"n": 10000, "d": 100, "precision": "fp32", "set_size": 10,
+            "l": 1, "kernel": "evaluate_single / greedy_maximize (public API)",
+            "kernel_s": t_single, "greedy_k10_s": t_greedy,
+            "greedy_picks": list(res.exemplar_indices),
+            "cand_sets_per_s": sum(10000 - t for t in range(10)) / t_greedy,
+            "alg_tflops": 0.0, "bound": "latency", "frac": float("nan")}
+
+
 def k4_case(n, d, prec_name, l, card, seed, pk):
     """Time K4 (explicit packed sets) through the evaluate_batch kernels."""
     import torch
@@ -157,7 +190,7 @@ def k4_case(n, d, prec_name, l, card, seed, pk):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="c2,c3,k4")
+    ap.add_argument("--only", default="c1,c2,c3,k4")
     ap.add_argument("--out", default="gpurun_out/sweep")
     ap.add_argument("--n", type=int, default=100_000)
     ap.add_argument("--dims", default="2,16,100,512,1024")
@@ -176,6 +209,8 @@ def main():
         recs.append(r)
         print(json.dumps(r), flush=True)
 
+    if "c1" in only:
+        emit("C1", c1_case())
     if "c2" in only:
         emit("C2", greedy_case(args.n, 100, "fp32", 19, 0, pk))
         emit("C2", greedy_case(args.n, 100, "fp32", 19, 0, pk, split32=True))
