@@ -140,7 +140,7 @@ struct MmaState {
 // (tools/k3_waits.sh, profiles/r01_k3_waits.log): WF = KS-2, WT = KS-1 is
 // 6 % faster than both before KS-2 (185.4 -> 173.5 ms); waiting for tempty
 // after the tile costs 25 %.
-template <int KS, int WF, int WT, typename P>
+template <int KS, int WF, int WT, bool MC, typename P>
 __device__ __forceinline__ void mma_item_waits(
     const P &p, int ntiles, MmaState &s, uint64_t a_desc0, uint64_t b_desc0,
     uint32_t stage_step, uint32_t tmem, uint64_t *full, uint64_t *empty,
@@ -176,7 +176,10 @@ __device__ __forceinline__ void mma_item_waits(
                b0 + (uint64_t)((ks >> 2) * kB + (ks & 3) * 2), p.idesc,
                ks > 0 ? 1u : 0u);
     }
-    umma_commit(&empty[s.stage]);
+    if constexpr (MC)
+      umma_commit_mc(&empty[s.stage], 3);  // both CTAs' B stage (multicast)
+    else
+      umma_commit(&empty[s.stage]);
     umma_commit(&tfull[s.buf]);
     if (WT == KS && more) {
       mbar_wait(&tempty[nbuf], ((s.tph >> nbuf) & 1u) ^ 1u);
@@ -230,10 +233,16 @@ struct Params {
   long long *trace;     // timing experiments only (EXEM_TC_TRACE)
 };
 
-template <bool kAStream>
+// kMC: 2-CTA cluster; the two CTAs score adjacent candidate tiles against
+// the same point tiles, each loading half of every B tile and multicasting
+// it to both (half the L2 -> SM traffic for B); a B stage is refilled only
+// when both CTAs' MMAs released it (empty barriers count 2, commits
+// multicast).  map_ph: the point operand with 128-row boxes.
+template <bool kAStream, bool kMC>
 __global__ void __launch_bounds__(kThreads, 1)
     gains_tc_kernel(const __grid_constant__ CUtensorMap map_c,
                     const __grid_constant__ CUtensorMap map_p,
+                    const __grid_constant__ CUtensorMap map_ph,
                     const Params p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-align the dynamic smem base (swizzle atoms).
@@ -259,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < p.stages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], kMC ? 2 : 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
@@ -279,18 +288,26 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   fence_before();
   __syncthreads();
+  if constexpr (kMC) cluster_sync();  // peers' barriers initialised
   fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  const int64_t items = p.cand_tiles * p.splits;
+  // work item = (split, candidate unit); a unit is one candidate tile, or
+  // with kMC a pair of adjacent tiles (CTA rank r of the cluster takes 2u+r)
+  const uint32_t crank = kMC ? cluster_rank() : 0u;
+  const int64_t cunits = kMC ? (p.cand_tiles + 1) / 2 : p.cand_tiles;
+  const int64_t wid = kMC ? blockIdx.x / 2 : blockIdx.x;
+  const int64_t nwork = kMC ? gridDim.x / 2 : gridDim.x;
+  const int64_t items = cunits * p.splits;
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
       int stage = 0;
       uint32_t ph = 0, aph = 0;
-      for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
-        const int64_t ct = it % p.cand_tiles, sp = it / p.cand_tiles;
+      for (int64_t it = wid; it < items; it += nwork) {
+        const int64_t ct = kMC ? 2 * (it % cunits) + crank : it % cunits;
+        const int64_t sp = it / cunits;
         const int crow = (int)(ct * BM);
         if (!kAStream) {
           mbar_wait(aempty, aph ^ 1);
@@ -309,6 +326,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             unsigned char *dst = sb + stage * stage_bytes;
             if (p.dbg & 4) {  // timing experiment: no operand traffic
               mbar_arrive(&full[stage]);
+            } else if (kMC) {
+              // this CTA's half of the B tile, to both CTAs of the pair
+              mbar_expect_tx(&full[stage], (uint32_t)stage_bytes);
+              for (int j = 0; j < per_stage; ++j)
+                tma_load_2d_mc(dst + j * B_CHUNK + crank * (B_CHUNK / 2),
+                               &map_ph, &full[stage], (kc0 + j) * KCH,
+                               (int)(pt + crank * (BN / 2)), 3);
             } else {
               mbar_expect_tx(&full[stage], (uint32_t)stage_bytes);
               for (int j = 0; j < per_stage; ++j)
@@ -340,8 +364,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t ph = 0, aph = 0, tph = 0;  // tph: bit b = phase of buffer b
       uint32_t buf = 0;
       int tile_no = 0;
-      for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
-        const int64_t sp = it / p.cand_tiles;
+      for (int64_t it = wid; it < items; it += nwork) {
+        const int64_t sp = it / cunits;
         if (!kAStream) {
           mbar_wait(afull, aph);
           aph ^= 1;
@@ -356,7 +380,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           switch (p.ksteps) {
 #define EXEM_K3_ITEM(K)                                                       \
   case K:                                                                     \
-    mma_item_waits<K, (K > 2 ? K - 2 : 0), (K > 1 ? K - 1 : 0)>(             \
+    mma_item_waits<K, (K > 2 ? K - 2 : 0), (K > 1 ? K - 1 : 0), kMC>(        \
         p, ntiles, ms, a_desc0, b_desc0, st_step, tmem, full, empty, tfull,   \
         tempty);                                                              \
     break;
@@ -404,7 +428,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                   }
               }
             }
-            if (!(p.dbg & 16)) umma_commit(&empty[stage]);
+            if (!(p.dbg & 16)) {
+              if constexpr (kMC) umma_commit_mc(&empty[stage], 3);
+              else umma_commit(&empty[stage]);
+            }
             if (++stage == p.stages) {
               stage = 0;
               ph ^= 1;
@@ -426,7 +453,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                            p.idesc, (kc | j) ? 1u : 0u);
               }
               ks_left -= KCH / 16;
-              umma_commit(&empty[stage]);
+              if constexpr (kMC) umma_commit_mc(&empty[stage], 3);
+              else umma_commit(&empty[stage]);
               if (++stage == p.stages) {
                 stage = 0;
                 ph ^= 1;
@@ -451,8 +479,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t buf = 0, tph = 0;  // tph: bit b = phase of buffer b
     int tile_no = 0;
     const bool tr = (warp == 2 && lane == 0);
-    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
-      const int64_t ct = it % p.cand_tiles, sp = it / p.cand_tiles;
+    for (int64_t it = wid; it < items; it += nwork) {
+      const int64_t ct = kMC ? 2 * (it % cunits) + crank : it % cunits;
+      const int64_t sp = it / cunits;
       const int64_t p0 = sp * p.split_pts;
       const int64_t p1 = min(p.n, p0 + p.split_pts);
       double g = 0.0;
@@ -521,6 +550,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   fence_before();
   __syncthreads();
+  if constexpr (kMC) cluster_sync();  // no multicast / commit still in flight
   if (warp == 1) {
     fence_after();
     asm volatile(
@@ -766,25 +796,65 @@ int exem_greedy_gains_tc(int dtype, const void *xc, int64_t l, const void *xp,
   CUtensorMap mc, mp;
   if (int rc = make_map(&mc, xc, dtype, exem_tc_rows(l), kp, BM)) return rc;
   if (int rc = make_map(&mp, xp, dtype, exem_tc_rows(n), kp, BN)) return rc;
-  const int64_t items = prm.cand_tiles * splits;
-  const unsigned grid = (unsigned)(items < sms ? items : sms);
+  CUtensorMap mph;  // 128-row boxes: one CTA's half of a B tile (kMC)
+  if (int rc = make_map(&mph, xp, dtype, exem_tc_rows(n), kp, BN / 2))
+    return rc;
+  // 2-CTA clusters sharing B tiles by TMA multicast (whole-tile stages, the
+  // pipelined issuer); EXEM_TC_MC=0 disables (timing experiments)
+  bool mcast = tile_stage && !astream && ksteps <= 8 && prm.dbg == 0;
+  if (const char *e = getenv("EXEM_TC_MC")) mcast = mcast && atoi(e) != 0;
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e;
-  if (astream) {
-    e = cudaFuncSetAttribute(gains_tc_kernel<true>,
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  if (mcast) {
+    e = cudaFuncSetAttribute(gains_tc_kernel<false, true>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
     if (e != cudaSuccess)
       return fail(EXEM_ERR_CUDA, "smem attr: %s", cudaGetErrorString(e));
-    gains_tc_kernel<true><<<grid, kThreads, smem, st>>>(mc, mp, prm);
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cfg.gridDim = dim3((unsigned)(sms & ~1));
+    int clusters = 0;
+    e = cudaOccupancyMaxActiveClusters(&clusters, gains_tc_kernel<false, true>,
+                                       &cfg);
+    if (e != cudaSuccess || clusters < 1)
+      return fail(EXEM_ERR_CUDA, "no co-resident CTA pairs: %s",
+                  cudaGetErrorString(e));
+    const int64_t units = (prm.cand_tiles + 1) / 2 * splits;
+    cfg.gridDim = dim3((unsigned)(2 * (units < clusters ? units : clusters)));
+    e = cudaLaunchKernelEx(&cfg, gains_tc_kernel<false, true>, mc, mp, mph,
+                           prm);
   } else {
-    e = cudaFuncSetAttribute(gains_tc_kernel<false>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-    if (e != cudaSuccess)
-      return fail(EXEM_ERR_CUDA, "smem attr: %s", cudaGetErrorString(e));
-    gains_tc_kernel<false><<<grid, kThreads, smem, st>>>(mc, mp, prm);
+    const int64_t items = prm.cand_tiles * splits;
+    cfg.gridDim = dim3((unsigned)(items < sms ? items : sms));
+    if (astream) {
+      e = cudaFuncSetAttribute(gains_tc_kernel<true, false>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem);
+      if (e == cudaSuccess)
+        e = cudaLaunchKernelEx(&cfg, gains_tc_kernel<true, false>, mc, mp,
+                               mph, prm);
+    } else {
+      e = cudaFuncSetAttribute(gains_tc_kernel<false, false>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem);
+      if (e == cudaSuccess)
+        e = cudaLaunchKernelEx(&cfg, gains_tc_kernel<false, false>, mc, mp,
+                               mph, prm);
+    }
   }
+  if (e != cudaSuccess)
+    return fail(EXEM_ERR_CUDA, "gains_tc_kernel launch: %s",
+                cudaGetErrorString(e));
   EXEM_LAUNCH_CHECK("gains_tc_kernel");
   if (prm.trace) {  // timing experiment: dump the CTA-0 timeline
     static long long host[16 * kTrace];

@@ -238,6 +238,27 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t *bar) {
       : "memory");
 }
 
+// TMA tile load multicast to the same smem offset (and the same mbarrier
+// offset) in every CTA of `mask` in the cluster.
+__device__ __forceinline__ void tma_load_2d_mc(void *dst, const CUtensorMap *map,
+                                               uint64_t *bar, int x, int y,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::"
+      "bytes.multicast::cluster [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(su32(dst)),
+      "l"((uint64_t)map), "r"(x), "r"(y), "r"(su32(bar)), "h"(mask)
+      : "memory");
+}
+// tcgen05.commit (cta_group::1) arriving on the mbarrier at this smem offset
+// in every CTA of `mask`.
+__device__ __forceinline__ void umma_commit_mc(uint64_t *bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster."
+      "multicast::cluster.b64 [%0], %1;" ::"r"(su32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
 #define TMEM_LD8(taddr, r)                                                    \
   asm volatile(                                                               \
       "tcgen05.ld.sync.aligned.32x32b.x8.b32 "                                \
