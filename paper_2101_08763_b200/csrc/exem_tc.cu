@@ -140,7 +140,7 @@ struct MmaState {
 // (tools/k3_waits.sh, profiles/r01_k3_waits.log): WF = KS-2, WT = KS-1 is
 // 6 % faster than both before KS-2 (185.4 -> 173.5 ms); waiting for tempty
 // after the tile costs 25 %.
-template <int KS, int WF, int WT, bool MC, typename P>
+template <int KS, int WF, int WT, int CS, typename P>
 __device__ __forceinline__ void mma_item_waits(
     const P &p, int ntiles, MmaState &s, uint64_t a_desc0, uint64_t b_desc0,
     uint32_t stage_step, uint32_t tmem, uint64_t *full, uint64_t *empty,
@@ -176,8 +176,8 @@ __device__ __forceinline__ void mma_item_waits(
                b0 + (uint64_t)((ks >> 2) * kB + (ks & 3) * 2), p.idesc,
                ks > 0 ? 1u : 0u);
     }
-    if constexpr (MC)
-      umma_commit_mc(&empty[s.stage], 3);  // both CTAs' B stage (multicast)
+    if constexpr (CS > 1)  // every cluster CTA's B stage (multicast)
+      umma_commit_mc(&empty[s.stage], (uint16_t)((1u << CS) - 1));
     else
       umma_commit(&empty[s.stage]);
     umma_commit(&tfull[s.buf]);
@@ -233,12 +233,13 @@ struct Params {
   long long *trace;     // timing experiments only (EXEM_TC_TRACE)
 };
 
-// kMC: 2-CTA cluster; the two CTAs score adjacent candidate tiles against
-// the same point tiles, each loading half of every B tile and multicasting
-// it to both (half the L2 -> SM traffic for B); a B stage is refilled only
-// when both CTAs' MMAs released it (empty barriers count 2, commits
-// multicast).  map_ph: the point operand with 128-row boxes.
-template <bool kAStream, bool kMC>
+// kCS > 1: kCS-CTA cluster; the CTAs score adjacent candidate tiles against
+// the same point tiles, each loading 1/kCS of every B tile and multicasting
+// it to all (1/kCS of the L2 -> SM traffic for B, less power, a higher
+// clock under the cap); a B stage is refilled only when every CTA's MMAs
+// released it (empty barriers count kCS, commits multicast).  map_ph: the
+// point operand with 256/kCS-row boxes.
+template <bool kAStream, int kCS>
 __global__ void __launch_bounds__(kThreads, 1)
     gains_tc_kernel(const __grid_constant__ CUtensorMap map_c,
                     const __grid_constant__ CUtensorMap map_p,
@@ -268,7 +269,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < p.stages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kMC ? 2 : 1);
+      mbar_init(&empty[s], kCS);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
@@ -288,16 +289,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   fence_before();
   __syncthreads();
-  if constexpr (kMC) cluster_sync();  // peers' barriers initialised
+  if constexpr (kCS > 1) cluster_sync();  // peers' barriers initialised
   fence_after();
   const uint32_t tmem = *tmem_slot;
 
   // work item = (split, candidate unit); a unit is one candidate tile, or
-  // with kMC a pair of adjacent tiles (CTA rank r of the cluster takes 2u+r)
-  const uint32_t crank = kMC ? cluster_rank() : 0u;
-  const int64_t cunits = kMC ? (p.cand_tiles + 1) / 2 : p.cand_tiles;
-  const int64_t wid = kMC ? blockIdx.x / 2 : blockIdx.x;
-  const int64_t nwork = kMC ? gridDim.x / 2 : gridDim.x;
+  // with clusters kCS adjacent tiles (CTA rank r of the cluster takes
+  // kCS*u + r)
+  const uint32_t crank = kCS > 1 ? cluster_rank() : 0u;
+  const int64_t cunits = (p.cand_tiles + kCS - 1) / kCS;
+  const int64_t wid = blockIdx.x / kCS;
+  const int64_t nwork = gridDim.x / kCS;
   const int64_t items = cunits * p.splits;
 
   if (warp == 0) {
@@ -306,7 +308,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t ph = 0, aph = 0;
       for (int64_t it = wid; it < items; it += nwork) {
-        const int64_t ct = kMC ? 2 * (it % cunits) + crank : it % cunits;
+        const int64_t ct = kCS * (it % cunits) + crank;
         const int64_t sp = it / cunits;
         const int crow = (int)(ct * BM);
         if (!kAStream) {
@@ -326,13 +328,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             unsigned char *dst = sb + stage * stage_bytes;
             if (p.dbg & 4) {  // timing experiment: no operand traffic
               mbar_arrive(&full[stage]);
-            } else if (kMC) {
-              // this CTA's half of the B tile, to both CTAs of the pair
+            } else if (kCS > 1) {
+              // this CTA's 1/kCS of the B tile, to every CTA of the cluster
               mbar_expect_tx(&full[stage], (uint32_t)stage_bytes);
               for (int j = 0; j < per_stage; ++j)
-                tma_load_2d_mc(dst + j * B_CHUNK + crank * (B_CHUNK / 2),
+                tma_load_2d_mc(dst + j * B_CHUNK + crank * (B_CHUNK / kCS),
                                &map_ph, &full[stage], (kc0 + j) * KCH,
-                               (int)(pt + crank * (BN / 2)), 3);
+                               (int)(pt + crank * (BN / kCS)),
+                               (uint16_t)((1u << kCS) - 1));
             } else {
               mbar_expect_tx(&full[stage], (uint32_t)stage_bytes);
               for (int j = 0; j < per_stage; ++j)
@@ -380,7 +383,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           switch (p.ksteps) {
 #define EXEM_K3_ITEM(K)                                                       \
   case K:                                                                     \
-    mma_item_waits<K, (K > 2 ? K - 2 : 0), (K > 1 ? K - 1 : 0), kMC>(        \
+    mma_item_waits<K, (K > 2 ? K - 2 : 0), (K > 1 ? K - 1 : 0), kCS>(        \
         p, ntiles, ms, a_desc0, b_desc0, st_step, tmem, full, empty, tfull,   \
         tempty);                                                              \
     break;
@@ -429,7 +432,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
             if (!(p.dbg & 16)) {
-              if constexpr (kMC) umma_commit_mc(&empty[stage], 3);
+              if constexpr (kCS > 1)
+                umma_commit_mc(&empty[stage], (uint16_t)((1u << kCS) - 1));
               else umma_commit(&empty[stage]);
             }
             if (++stage == p.stages) {
@@ -453,7 +457,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                            p.idesc, (kc | j) ? 1u : 0u);
               }
               ks_left -= KCH / 16;
-              if constexpr (kMC) umma_commit_mc(&empty[stage], 3);
+              if constexpr (kCS > 1)
+                umma_commit_mc(&empty[stage], (uint16_t)((1u << kCS) - 1));
               else umma_commit(&empty[stage]);
               if (++stage == p.stages) {
                 stage = 0;
@@ -480,7 +485,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int tile_no = 0;
     const bool tr = (warp == 2 && lane == 0);
     for (int64_t it = wid; it < items; it += nwork) {
-      const int64_t ct = kMC ? 2 * (it % cunits) + crank : it % cunits;
+      const int64_t ct = kCS * (it % cunits) + crank;
       const int64_t sp = it / cunits;
       const int64_t p0 = sp * p.split_pts;
       const int64_t p1 = min(p.n, p0 + p.split_pts);
@@ -550,7 +555,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   fence_before();
   __syncthreads();
-  if constexpr (kMC) cluster_sync();  // no multicast / commit still in flight
+  if constexpr (kCS > 1) cluster_sync();  // no multicast / commit in flight
   if (warp == 1) {
     fence_after();
     asm volatile(
@@ -796,13 +801,16 @@ int exem_greedy_gains_tc(int dtype, const void *xc, int64_t l, const void *xp,
   CUtensorMap mc, mp;
   if (int rc = make_map(&mc, xc, dtype, exem_tc_rows(l), kp, BM)) return rc;
   if (int rc = make_map(&mp, xp, dtype, exem_tc_rows(n), kp, BN)) return rc;
-  CUtensorMap mph;  // 128-row boxes: one CTA's half of a B tile (kMC)
-  if (int rc = make_map(&mph, xp, dtype, exem_tc_rows(n), kp, BN / 2))
+  // clusters sharing B tiles by TMA multicast (whole-tile stages, the
+  // pipelined issuer): cluster size 2 by default, EXEM_TC_MC = 0 | 1 | 2 | 4
+  // (0/1: none) for timing experiments
+  int cs = (tile_stage && !astream && ksteps <= 8 && prm.dbg == 0) ? 2 : 1;
+  if (const char *e = getenv("EXEM_TC_MC"))
+    if (cs > 1) cs = atoi(e) >= 4 ? 4 : (atoi(e) >= 2 ? 2 : 1);
+  const bool mcast = cs > 1;
+  CUtensorMap mph;  // 256/cs-row boxes: one CTA's share of a B tile
+  if (int rc = make_map(&mph, xp, dtype, exem_tc_rows(n), kp, BN / cs))
     return rc;
-  // 2-CTA clusters sharing B tiles by TMA multicast (whole-tile stages, the
-  // pipelined issuer); EXEM_TC_MC=0 disables (timing experiments)
-  bool mcast = tile_stage && !astream && ksteps <= 8 && prm.dbg == 0;
-  if (const char *e = getenv("EXEM_TC_MC")) mcast = mcast && atoi(e) != 0;
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e;
   cudaLaunchConfig_t cfg = {};
@@ -811,44 +819,42 @@ int exem_greedy_gains_tc(int dtype, const void *xc, int64_t l, const void *xp,
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   if (mcast) {
-    e = cudaFuncSetAttribute(gains_tc_kernel<false, true>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+    auto kern = cs == 4 ? gains_tc_kernel<false, 4> : gains_tc_kernel<false, 2>;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
     if (e != cudaSuccess)
       return fail(EXEM_ERR_CUDA, "smem attr: %s", cudaGetErrorString(e));
     at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.x = cs;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    cfg.gridDim = dim3((unsigned)(sms & ~1));
+    cfg.gridDim = dim3((unsigned)(sms / cs * cs));
     int clusters = 0;
-    e = cudaOccupancyMaxActiveClusters(&clusters, gains_tc_kernel<false, true>,
-                                       &cfg);
+    e = cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg);
     if (e != cudaSuccess || clusters < 1)
-      return fail(EXEM_ERR_CUDA, "no co-resident CTA pairs: %s",
+      return fail(EXEM_ERR_CUDA, "no co-resident CTA clusters: %s",
                   cudaGetErrorString(e));
-    const int64_t units = (prm.cand_tiles + 1) / 2 * splits;
-    cfg.gridDim = dim3((unsigned)(2 * (units < clusters ? units : clusters)));
-    e = cudaLaunchKernelEx(&cfg, gains_tc_kernel<false, true>, mc, mp, mph,
-                           prm);
+    const int64_t units = (prm.cand_tiles + cs - 1) / cs * splits;
+    cfg.gridDim = dim3((unsigned)(cs * (units < clusters ? units : clusters)));
+    e = cudaLaunchKernelEx(&cfg, kern, mc, mp, mph, prm);
   } else {
     const int64_t items = prm.cand_tiles * splits;
     cfg.gridDim = dim3((unsigned)(items < sms ? items : sms));
     if (astream) {
-      e = cudaFuncSetAttribute(gains_tc_kernel<true, false>,
+      e = cudaFuncSetAttribute(gains_tc_kernel<true, 1>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)smem);
       if (e == cudaSuccess)
-        e = cudaLaunchKernelEx(&cfg, gains_tc_kernel<true, false>, mc, mp,
+        e = cudaLaunchKernelEx(&cfg, gains_tc_kernel<true, 1>, mc, mp,
                                mph, prm);
     } else {
-      e = cudaFuncSetAttribute(gains_tc_kernel<false, false>,
+      e = cudaFuncSetAttribute(gains_tc_kernel<false, 1>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)smem);
       if (e == cudaSuccess)
-        e = cudaLaunchKernelEx(&cfg, gains_tc_kernel<false, false>, mc, mp,
+        e = cudaLaunchKernelEx(&cfg, gains_tc_kernel<false, 1>, mc, mp,
                                mph, prm);
     }
   }
