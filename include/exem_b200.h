@@ -107,6 +107,17 @@ int exem_h2d_rows(void *dst, const void *host, int64_t ld_host, int64_t row0,
 int exem_sum_fixed(const double *in, int64_t count, double *out,
                    int64_t out_index, void *stream);
 
+/* K1 for a ROW-major source src[n][d] (a C-order numpy matrix uploaded as
+ * is, no host transpose); outputs and aux block partials bit-identical to
+ * exem_ground_prepare. */
+int exem_ground_prepare_rows(int dtype, const void *src, int64_t n, int64_t d,
+                             const void *e0, void *vt, int64_t ld,
+                             double *norms, void *aux, double *aux_sum,
+                             double *scratch, void *stream);
+/* Plain async host -> device copy (a contiguous row slice of a row-major
+ * host matrix in the low-memory regime). */
+int exem_h2d_bytes(void *dst, const void *host, int64_t bytes, void *stream);
+
 /*
  * K2  set_min -- per-point minimum over one explicit element set
  * Replaces min_distances, pkg/src/exembatch/objective.py:113-141, and the

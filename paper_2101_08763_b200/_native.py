@@ -102,6 +102,9 @@ _SIGNATURES = {
     "exem_peer_argmax_select": (c_int, [_P, _P, c_int, ctypes.c_uint64,
                                         c_int64, c_double, _P, _P, c_int64,
                                         _P, _P, _P, _P]),
+    "exem_ground_prepare_rows": (c_int, [c_int, _P, c_int64, c_int64, _P, _P,
+                                         c_int64, _P, _P, _P, _P, _P]),
+    "exem_h2d_bytes": (c_int, [_P, _P, c_int64, _P]),
     "exem_launch_count": (c_int64, []),
 }
 

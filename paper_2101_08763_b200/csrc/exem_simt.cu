@@ -103,6 +103,70 @@ __global__ void __launch_bounds__(kRedThreads)
   if (threadIdx.x == 0) partials[blockIdx.x] = r;
 }
 
+// K1 for a row-major source (src[i][k], the C-order numpy matrix uploaded
+// as is): the block's 256 points are staged through shared memory 32
+// dimensions at a time (coalesced reads of the rows, conflict-free column
+// reads with a 33-element row pitch), then exactly the per-point arithmetic
+// and block partials of ground_prepare_kernel -- results are bit-identical
+// to the column-major path.
+template <int DT>
+__global__ void __launch_bounds__(kRedThreads)
+    ground_prepare_rows_kernel(const typename Traits<DT>::S *__restrict__ src,
+                               int64_t n, int d, int d_pad,
+                               const typename Traits<DT>::S *__restrict__ e0,
+                               typename Traits<DT>::C *__restrict__ vt,
+                               int64_t ld, double *__restrict__ norms,
+                               typename Traits<DT>::C *__restrict__ aux,
+                               double *__restrict__ partials) {
+  using S = typename Traits<DT>::S;
+  using C = typename Traits<DT>::C;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C(*tile)[33] = reinterpret_cast<C(*)[33]>(smem_raw);  // [256][33]
+  __shared__ double sh[32];
+  const int64_t i0 = (int64_t)blockIdx.x * blockDim.x;
+  const int64_t i = i0 + threadIdx.x;
+  double nrm = 0.0, dst = 0.0;
+  for (int k0 = 0; k0 < d_pad; k0 += 32) {
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < kRedThreads * 32; idx += kRedThreads) {
+      const int pp = idx >> 5, kk = idx & 31;
+      const int64_t ip = i0 + pp;
+      const int k = k0 + kk;
+      tile[pp][kk] = (k < d && ip < n) ? to_c(src[ip * d + k]) : C(0);
+    }
+    __syncthreads();
+    if (i < ld) {
+      for (int kk = 0; kk < 32 && k0 + kk < d_pad; ++kk) {
+        const int k = k0 + kk;
+        const C x = tile[threadIdx.x][kk];
+        vt[(int64_t)k * ld + i] = x;
+        if (k < d && i < n) {
+          double xd = (double)x;
+          nrm += xd * xd;
+          double df = xd - (double)to_c(e0[k]);
+          dst += df * df;
+        }
+      }
+    }
+  }
+  if (i < ld) {
+    C a = C(0);
+    if (i < n) a = (DT == EXEM_BF16) ? (C)dst : to_c(from_d<S>(dst));
+    if (i < n) {
+      norms[i] = nrm;
+      aux[i] = a;
+    } else {
+      norms[i] = 0.0;
+      aux[i] = C(0);
+    }
+    dst = (i < n) ? (double)a : 0.0;
+  } else {
+    dst = 0.0;
+  }
+  double r = block_sum<kRedThreads>(dst, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = r;
+}
+
 // ============================================================ K2 set_min
 // One thread per point; the set's elements are staged through shared memory
 // in chunks of kSetChunk rows and each thread keeps kSetChunk dot products in
@@ -1259,6 +1323,45 @@ int exem_peer_argmax_select(const double *const *peers,
                                                  nullptr, step, sel_idx,
                                                  sel_gain);
   EXEM_LAUNCH_CHECK("argmax_final_kernel");
+  return EXEM_OK;
+}
+
+int exem_ground_prepare_rows(int dtype, const void *src, int64_t n, int64_t d,
+                             const void *e0, void *vt, int64_t ld,
+                             double *norms, void *aux, double *aux_sum,
+                             double *scratch, void *stream) {
+  if (n < 1 || d < 1 || ld < n || ld % kPointPad)
+    return fail(EXEM_ERR_ARG, "ground_prepare_rows: bad shape");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int d_pad = (int)exem_pad_dims(d);
+  const int64_t blocks = ceil_div(ld, kRedThreads);
+  EXEM_DISPATCH(dtype, DT, {
+    using S = typename Traits<DT>::S;
+    using C = typename Traits<DT>::C;
+    const size_t smem = (size_t)kRedThreads * 33 * sizeof(C);
+    if (smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(
+          ground_prepare_rows_kernel<DT>,
+          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess)
+        return fail(EXEM_ERR_CUDA, "prepare_rows smem: %s",
+                    cudaGetErrorString(e));
+    }
+    ground_prepare_rows_kernel<DT><<<(unsigned)blocks, kRedThreads, smem, st>>>(
+        (const S *)src, n, (int)d, d_pad, (const S *)e0, (C *)vt, ld, norms,
+        (C *)aux, scratch);
+    EXEM_LAUNCH_CHECK("ground_prepare_rows_kernel");
+  });
+  if (!aux_sum) return EXEM_OK;
+  return reduce_fixed(scratch, blocks, aux_sum, 0, st);
+}
+
+int exem_h2d_bytes(void *dst, const void *host, int64_t bytes, void *stream) {
+  if (bytes < 1) return EXEM_OK;
+  cudaError_t e = cudaMemcpyAsync(dst, host, (size_t)bytes,
+                                  cudaMemcpyHostToDevice, (cudaStream_t)stream);
+  if (e != cudaSuccess)
+    return fail(EXEM_ERR_CUDA, "h2d_bytes: %s", cudaGetErrorString(e));
   return EXEM_OK;
 }
 

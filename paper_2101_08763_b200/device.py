@@ -172,20 +172,34 @@ class DeviceGround:
         return self._xc
 
 
+def row_major(matrix: np.ndarray) -> bool:
+    """True when the host matrix is C-order (and not also F-order)."""
+    return bool(matrix.flags.c_contiguous and not matrix.flags.f_contiguous)
+
+
 def prepare_ground(matrix: np.ndarray, aux_vec: np.ndarray, precision,
                    device=None):
-    """Run K1 on the uploaded F-order buffer; return (state, aux_dist, sum)."""
+    """Upload V in its host layout and run K1 (column-major, the reference's
+    layout, or row-major); return (state, aux_dist, sum)."""
     t = torch()
     idx = require_cuda(device)
     lib = N.lib()
     n, d = matrix.shape
     with t.cuda.device(idx):
         dg = DeviceGround(n, d, precision, idx)
-        src = to_device_bytes(matrix.ravel(order="F"), dg.dev)
         e0 = to_device_bytes(aux_vec, dg.dev)
-        lib.ground_prepare(precision.tag, N.ptr(src), n, d, N.ptr(e0),
-                           N.ptr(dg.vt), dg.ld, N.ptr(dg.norms), N.ptr(dg.aux),
-                           N.ptr(dg.aux_sum), N.ptr(dg.scratch), dg.stream)
+        if not (matrix.flags.c_contiguous or matrix.flags.f_contiguous):
+            matrix = np.asfortranarray(matrix)
+        # one DMA straight from the (read-only, frozen) host matrix: no
+        # host-side staging copy; row-major sources are transposed by K1
+        src = t.empty(max(matrix.nbytes, 1), dtype=t.uint8, device=dg.dev)
+        lib.h2d_bytes(N.ptr(src), N.c_void_p(matrix.ctypes.data),
+                      matrix.nbytes, dg.stream)
+        prepare = (lib.ground_prepare_rows if row_major(matrix)
+                   else lib.ground_prepare)
+        prepare(precision.tag, N.ptr(src), n, d, N.ptr(e0), N.ptr(dg.vt),
+                dg.ld, N.ptr(dg.norms), N.ptr(dg.aux), N.ptr(dg.aux_sum),
+                N.ptr(dg.scratch), dg.stream)
         aux_host = dg.aux[:n].cpu().numpy().astype(aux_dtype(precision))
         aux_sum = float(dg.aux_sum.item())
         del src, e0

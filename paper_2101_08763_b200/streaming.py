@@ -195,8 +195,11 @@ class GroundStream:
             raise ValueError("a streamed row range must start on a split")
         self.plan = plan_slices(self.row1 - self.row0, self.d, self.prec,
                                 free_bytes, self.split_pts)
+        from .device import row_major
+
         host = ground.matrix
-        assert host.flags.f_contiguous
+        self.row_major = row_major(host)
+        assert self.row_major or host.flags.f_contiguous
         self._host_ptr = c_void_p(host.ctypes.data)
         with t.cuda.device(self.idx):
             pin_host(ground)
@@ -212,6 +215,26 @@ class GroundStream:
     def close(self):
         """Release the ring (the host pages stay locked for reuse)."""
         self.slots = []
+
+    def upload(self, dst, r0: int, rows: int, stream) -> None:
+        """Rows [r0, r0+rows) of the host matrix -> the device staging
+        buffer, in the host's own layout (2-D DMA of a column-major slice,
+        or one contiguous copy of a row-major slice)."""
+        bpv = self.prec.bytes_per_value
+        if self.row_major:
+            self.lib.h2d_bytes(N.ptr(dst), c_void_p(self._host_ptr.value +
+                                                    r0 * self.d * bpv),
+                               rows * self.d * bpv, stream)
+        else:
+            self.lib.h2d_rows(N.ptr(dst), self._host_ptr, self.n, r0, rows,
+                              self.d, bpv, stream)
+
+    def prepare(self, src, rows, vt, ld, norms, aux, partials, stream):
+        """K1 on an uploaded slice (row- or column-major source)."""
+        fn = (self.lib.ground_prepare_rows if self.row_major
+              else self.lib.ground_prepare)
+        fn(self.prec.tag, src, rows, self.d, N.ptr(self.e0), vt, ld, norms,
+           aux, None, partials, stream)
 
     def block_ptr(self, r0: int) -> c_void_p:
         return c_void_p(self.block_partials.data_ptr() + (r0 // 256) * 8)
@@ -231,17 +254,14 @@ class GroundStream:
                 cs = self.copy_stream
                 cs.wait_event(slot.consumed)  # K1 of the slot's last use done
                 with t.cuda.stream(cs):
-                    lib.h2d_rows(N.ptr(slot.src), self._host_ptr, self.n, r0,
-                                 rows, self.d, prec.bytes_per_value,
-                                 c_void_p(cs.cuda_stream))
+                    self.upload(slot.src, r0, rows, c_void_p(cs.cuda_stream))
                     slot.uploaded.record(cs)
                 compute.wait_event(slot.uploaded)
                 slot.n = rows
                 slot.ld = int(lib.pad_points(rows))
-                lib.ground_prepare(prec.tag, N.ptr(slot.src), rows, self.d,
-                                   N.ptr(self.e0), N.ptr(slot.vt), slot.ld,
-                                   N.ptr(slot.norms), N.ptr(slot.aux), None,
-                                   self.block_ptr(r0), st)
+                self.prepare(N.ptr(slot.src), rows, N.ptr(slot.vt), slot.ld,
+                             N.ptr(slot.norms), N.ptr(slot.aux),
+                             self.block_ptr(r0), st)
                 slot.consumed.record(compute)
                 if prec.is_half and pack_points:
                     if slot.plain:
@@ -445,16 +465,13 @@ def stream_greedy(ground, k: int, device=None):
                 tdt = t.bfloat16 if prec.tag == N.BF16 else t.float16
                 c_xc = t.empty((int(lib.tc_rows(cand_rows)),
                                 int(lib.tc_kp(d))), dtype=tdt, device=dev)
-            host_ptr = gs._host_ptr
 
             def load_candidates(c0, c1):
                 rows = c1 - c0
-                lib.h2d_rows(N.ptr(c_src), host_ptr, n, c0, rows, d,
-                             prec.bytes_per_value, st)
-                lib.ground_prepare(prec.tag, N.ptr(c_src), rows, d,
-                                   N.ptr(gs.e0), N.ptr(c_vt),
-                                   int(lib.pad_points(rows)), N.ptr(c_norms),
-                                   N.ptr(c_aux), None, N.ptr(scratch), st)
+                gs.upload(c_src, c0, rows, st)
+                gs.prepare(N.ptr(c_src), rows, N.ptr(c_vt),
+                           int(lib.pad_points(rows)), N.ptr(c_norms),
+                           N.ptr(c_aux), N.ptr(scratch), st)
                 if half:
                     lib.tc_pack_candidates(prec.tag, N.ptr(c_vt),
                                            int(lib.pad_points(rows)), rows, d,

@@ -126,3 +126,36 @@ def test_streamed_greedy_matches_resident(prec):
     assert res.values == ref.values
     assert res.evaluations == ref.evaluations
     assert sp > 0
+
+
+@pytest.mark.parametrize("prec", [P32, P64, BF16, P16])
+def test_row_major_input_matches_column_major(prec):
+    """A C-order input is uploaded untransposed and K1's row-major variant
+    (exem_ground_prepare_rows) transposes on the device; everything derived
+    from it -- aux distances, L({e0}), batch sums, Greedy -- is bit-identical
+    to the column-major (reference layout) path, resident and streamed."""
+    rng = np.random.default_rng(5)
+    n, d, l, k = 20_003, 45, 40, 3
+    data = rng.standard_normal((n, d)) * (0.5 if prec is P16 else 1.0)
+    rows = np.ascontiguousarray(data.astype(prec.dtype))
+    cols = np.asfortranarray(rows)
+    idx = [np.sort(rng.choice(n, size=int(rng.integers(1, 11)), replace=False))
+           for _ in range(l)]
+    budget = _budget(n, d, prec, l, 10)
+    ref = None
+    for src in (cols, rows):
+        for kw in ({}, {"device_budget": budget}):
+            g = pb.build_ground_set(src, precision=prec, **kw)
+            assert g.matrix.flags.c_contiguous == (src is rows)
+            b = EvaluationBatch.from_sets([g.matrix[i] for i in idx])
+            got = (g.aux_loss, g.aux_distances.copy(),
+                   pb.evaluate_batch(Evaluator(), g, b),
+                   pb.greedy_maximize(g, k=k))
+            if ref is None:
+                ref = got
+                continue
+            assert got[0] == ref[0]
+            assert np.array_equal(got[1], ref[1])
+            assert np.array_equal(got[2], ref[2])
+            assert got[3].exemplar_indices == ref[3].exemplar_indices
+            assert got[3].values == ref[3].values

@@ -81,6 +81,13 @@ def main():
             N.ptr(dg.scratch), st))
         rec(f"K1 ground_prepare ({prec.value})",
             n * d * prec.bytes_per_value + n * dg.d_pad * 4 + 16 * n, t)
+        src_r = to_device_bytes(np.ascontiguousarray(g.matrix), dg.dev)
+        t = timed(lambda: lib.ground_prepare_rows(
+            prec.tag, N.ptr(src_r), n, d, N.ptr(e0), N.ptr(dg.vt), dg.ld,
+            N.ptr(dg.norms), N.ptr(dg.aux), N.ptr(dg.aux_sum),
+            N.ptr(dg.scratch), st))
+        rec(f"K1 ground_prepare_rows ({prec.value}, row-major source)",
+            n * d * prec.bytes_per_value + n * dg.d_pad * 4 + 16 * n, t)
         if prec is not pb.Precision.binary32:
             continue
         for k in (1, 10, 50):
