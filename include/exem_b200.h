@@ -198,9 +198,10 @@ int exem_greedy_gains_tc(int dtype, const void *xc, int64_t l, const void *xp,
  *        m = NULL (h_i = ||v_i||^2 / 2).
  *   aux  [n] float aux distances (compute type).
  *   xs   [tc_set_rows(l, k_max)][kp] set-tile operand (exem_tc_pack_sets).
- * exem_tc_set_geometry: a set tile holds `spt` sets of `w` = round_up(k_max,
- * 8) columns, MMA N = ncols; EXEM_ERR_UNSUPPORTED when k_max > 256 (the
- * caller then uses exem_batch_eval).
+ * exem_tc_set_geometry: a set tile holds `spt` = min(16, 256 / k_max) sets
+ * of `w` = k_max slots, column-interleaved (column c = slot c / spt of set
+ * c % spt), MMA N = ncols = round_up(spt * w, 16); EXEM_ERR_UNSUPPORTED when
+ * k_max > 256 (the caller then uses exem_batch_eval).
  */
 int exem_tc_set_geometry(int64_t k_max, int32_t *spt, int32_t *w,
                          int32_t *ncols);

@@ -16,10 +16,13 @@
 //
 // Operand roles: points on M (TMEM lanes, streamed by TMA per K chunk),
 // set elements on N (the "set tile", stationary in smem for a work item).
-// A set tile holds `spt` whole sets, each padded to `w` = round_up(k_max, 8)
-// columns; blank slots (e >= card_j) and padding columns are copies of the
-// set's element 0, so they never change a minimum and need no masking
-// (cf. the blank-slot rule, core.py:227-230).
+// A set tile holds `spt` = min(16, 256 / k_max) sets, column-interleaved:
+// column c is slot c / spt of set c % spt (the packed batch's own round-robin
+// order, core.py:331-346), so N = round_up(spt * k_max, 16) with no per-set
+// padding (k_max = 50: 5 sets in N = 256, not 4 in 224).  Blank slots
+// (e >= card_j) and padding columns are copies of the set's element 0, so
+// they never change a minimum and need no masking (cf. the blank-slot rule,
+// core.py:227-230).
 //
 // Roles (320 threads, 1 CTA/SM, persistent over (split, set tile) items):
 //   warp 0      TMA producer (set tile once per item; point K-chunks
@@ -28,8 +31,8 @@
 //               N=ncols x K=16), handshakes software-pipelined one chunk
 //               ahead so the tensor pipe's ~2-deep queue never drains
 //   warps 2-9   epilogue: lane quarter q = warp%4 (TMEM lane access rule),
-//               set parity h = (warp-2)/4; per-thread fp64 running sums per
-//               set across the item's point tiles, fixed-order xor-shuffle +
+//               column-group / set parity h = (warp-2)/4 (maxima swapped
+//               through smem); per-thread fp64 running sums per set across the item's point tiles, fixed-order xor-shuffle +
 //               cross-quarter reduction at item end (deterministic).
 #include <cstdlib>
 
@@ -46,7 +49,8 @@ constexpr int kThreads = 320;
 constexpr int kEpiWarps = 8;
 constexpr int kMaxSpt = 16;             // sets per set tile (register budget of the epilogue)
 constexpr int kSmemBudget = 227 * 1024;
-constexpr int kBarBytes = 3072;  // barriers, reductions, plain b
+constexpr int kXchBytes = 2 * kMaxSpt * BM * 4;  // epilogue max exchange
+constexpr int kBarBytes = 3072 + kXchBytes;  // barriers, reductions, plain b, exchange
 constexpr int kTrace = 256;  // tiles traced on CTA 0
 // CTA-0 timeline for timing experiments (tools/tcb_trace.py): compiled in
 // only with -DEXEM_TCB_TRACE_BUILD (EXEM_NVCC_FLAGS at build time) -- the
@@ -70,7 +74,7 @@ struct BParams {
   int64_t splits;
   int64_t set_tiles;
   int spt;             // sets per set tile
-  int w;               // TMEM columns per set (multiple of 8)
+  int w;               // slots per set (= k_max; columns interleaved)
   int ncols;           // MMA N (multiple of 16, >= spt * w)
   int ksteps;          // K=16 MMA steps
   int kchunks;         // 64-wide K chunks per operand row
@@ -79,6 +83,7 @@ struct BParams {
   int tstage;          // 1: a ring stage holds a whole point tile (all K)
   int gch;             // otherwise: 64-wide K chunks per ring stage (1, 2)
   int dbg;             // timing experiments only (EXEM_TCB_DEBUG), 0 in use
+  int late;            // 1: next accumulator buffer acquired after the commit
   uint32_t idesc;
   long long *trace;    // timing experiments only (EXEM_TCB_TRACE): CTA-0 timeline
   const float *aux;    // [n] aux distances (compute type)
@@ -88,177 +93,139 @@ struct BParams {
   double *partial;     // [splits][l]
 };
 
-__device__ __forceinline__ float max8(const uint32_t (&r)[8], float m) {
-#pragma unroll
-  for (int j = 0; j < 8; ++j) m = fmaxf(m, __uint_as_float(r[j]));
-  return m;
-}
+// Work items (split sp, set tile st) of one CTA.  A cluster of MC CTAs takes
+// units (split, group of MC adjacent set tiles): CTA rank r scores set tile
+// MC*g + r against the SAME point tiles, which are multicast to all MC CTAs
+// (each CTA loads 1/MC of every point chunk: 1/MC of the L2 -> SM traffic).
+// A spare tile (st >= set_tiles, odd set_tiles) reads TMA's zero fill and
+// writes nothing.
+struct WorkSplit {
+  int64_t first, step, units, groups;  // groups = ceil(set_tiles / MC)
+  int mc;
+  uint32_t rank;
+  __device__ __forceinline__ void item(int64_t u, int64_t &st,
+                                       int64_t &sp) const {
+    sp = u / groups;
+    st = (int64_t)mc * (u % groups) + rank;
+  }
+};
 
-// Release an accumulator buffer once every lane's tcgen05.ld is complete:
-// on this CTA's tempty (CG = 1) or on the pair leader's (CG = 2).
-template <int CG>
+// Release an accumulator buffer once every lane's tcgen05.ld is complete.
 struct TmemRelease {
   uint64_t *bar;
   int lane;
   __device__ __forceinline__ void operator()() const {
     fence_before();
     __syncwarp();
-    if (lane == 0) {
-      if constexpr (CG == 2)
-        mbar_arrive_cluster(mapa(bar, 0));
-      else
-        mbar_arrive(bar);
-    }
+    if (lane == 0) mbar_arrive(bar);
   }
 };
 
-// Epilogue of one accumulator tile for one warp, set width W8*8 columns known
-// at compile time.  The warp owns sets s = h + 2u (u < nsets); their columns
-// are drained with tcgen05.ld x8 into registers in batches of sets
-// (EpiShape) and ONE tcgen05.wait::ld per batch -- the TMEM load
-// latency is paid once per tile, not once per 32 columns -- and the buffer is
-// released right after the last batch's wait, before its arithmetic.
+// Epilogue of one accumulator tile for one warp.  Set tiles are column-
+// interleaved: column c holds slot c / SPT of set c % SPT (exem_tc_pack_sets),
+// so with SPT known at compile time every column's set is static.  The two
+// warps of a TMEM lane quarter split the tile's 8-column groups (g = 2i + HH,
+// an even split for any N), each folds its columns into per-set maxima pm[],
+// and they swap the maxima of the sets the other one owns (set parity) through
+// shared memory -- one 64-thread named barrier per tile.  Columns are drained
+// with tcgen05.ld x8 in batches of 8 groups and one tcgen05.wait::ld per
+// batch; the buffer is released right after the last batch's wait.
 //   t = min(aux_i, max(0, -2 max_e D)),  acc[u] += t   (fp64, per thread)
-template <int W8>
+template <int SPT>
 struct EpiShape {
-  static constexpr int SPT = 32 / W8 < kMaxSpt ? 32 / W8 : kMaxSpt;
-  static constexpr int MAXS = (SPT + 1) / 2;  // sets per warp (max)
-  // sets per load batch: registers of one batch (8 per group) plus the fp64
-  // accumulators within a 116-register budget (ptxas caps this kernel at
-  // 168 registers per thread)
-  static constexpr int sb() {
-    int best = 1;
-    for (int s = 1; s <= MAXS; ++s)
-      if (s * W8 * 8 + 2 * MAXS <= 116) best = s;
-    return best;
-  }
-  static constexpr int SB = sb();
-  static constexpr int NB = (MAXS + SB - 1) / SB;
+  static constexpr int OWN = (SPT + 1) / 2;  // sets finalised per warp (max)
+  static constexpr int GB = 8;               // 8-column groups per ld batch
 };
 
-// max over 8 columns of D - b[col] (plain operands: b = ||e||^2/2 of the
-// column's element, from shared memory)
-__device__ __forceinline__ float max8b(const uint32_t (&r)[8], const float *b,
-                                       float m) {
-#pragma unroll
-  for (int j = 0; j < 8; ++j) m = fmaxf(m, __uint_as_float(r[j]) - b[j]);
-  return m;
-}
-
-template <int W8, bool kPlain, typename Release>
+// xch: this buffer's [kMaxSpt][BM] exchange slots (set-major, row-minor:
+// conflict-free).
+template <int SPT, int HH, bool kPlain, typename Release>
 __device__ __forceinline__ void epi_tile(
-    uint32_t taddr, int h, int spt, int w, float ax, float ha, bool valid,
-    const float *bsm, double (&acc)[EpiShape<W8>::MAXS],
-    const Release &release) {
+    uint32_t taddr, int ngroups, int q, int row, float ax, float ha,
+    bool valid, const float *bsm, float *xch,
+    double (&acc)[EpiShape<SPT>::OWN], const Release &release) {
+  constexpr int GB = EpiShape<SPT>::GB;
   const float ninf = -__int_as_float(0x7f800000);
-  const int nsets = (spt - h + 1) >> 1;
-  if (nsets <= 0) {
-    release();
-    return;
-  }
-  if constexpr (W8 * 8 + 2 * EpiShape<W8>::MAXS <= 116) {
-    constexpr int SB = EpiShape<W8>::SB;
-    constexpr int NB = EpiShape<W8>::NB;
-    const int nbat = (nsets + SB - 1) / SB;
+  float pm[SPT];
 #pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      if (b < nbat) {
-        uint32_t r[SB * W8][8];
+  for (int s = 0; s < SPT; ++s) pm[s] = ninf;
+  const int mine = (ngroups - HH + 1) >> 1;  // this warp's groups (>= 1)
 #pragma unroll
-        for (int j = 0; j < SB; ++j) {
-          if (b * SB + j < nsets) {
-            const uint32_t c0 = taddr + (uint32_t)((h + 2 * (b * SB + j)) * w);
+  for (int b = 0; b < 16 / GB; ++b) {
+    if (b * GB < mine) {
+      uint32_t r[GB][8];
 #pragma unroll
-            for (int g = 0; g < W8; ++g) TMEM_LD8(c0 + 8 * g, r[j * W8 + g]);
-          }
-        }
-        tmem_wait_ld();
-        if (b == nbat - 1) release();
+      for (int i = 0; i < GB; ++i)
+        if (b * GB + i < mine)
+          TMEM_LD8(taddr + (uint32_t)(8 * (2 * (b * GB + i) + HH)), r[i]);
+      tmem_wait_ld();
+      if ((b + 1) * GB >= mine) release();
 #pragma unroll
-        for (int j = 0; j < SB; ++j) {
-          if (b * SB + j < nsets) {
-            float mx = ninf;
-            const int cb = (h + 2 * (b * SB + j)) * w;  // set's first column
+      for (int i = 0; i < GB; ++i) {
+        if (b * GB + i < mine) {
 #pragma unroll
-            for (int g = 0; g < W8; ++g)
-              mx = kPlain ? max8b(r[j * W8 + g], bsm + cb + 8 * g, mx)
-                          : max8(r[j * W8 + g], mx);
-            // folded: min_e d = -2 max D;  plain: min_e d = a - 2 max (D - b)
-            const float dm = kPlain ? fmaf(-2.f, mx, ha) : -2.f * mx;
-            const float t = fminf(ax, fmaxf(0.f, dm));
-            if (valid) acc[b * SB + j] += (double)t;
+          for (int k = 0; k < 8; ++k) {
+            const int c = 8 * (2 * (b * GB + i) + HH) + k;  // static
+            float v = __uint_as_float(r[i][k]);
+            if constexpr (kPlain) v -= bsm[c];
+            pm[c % SPT] = fmaxf(pm[c % SPT], v);
           }
         }
       }
     }
-  } else {
-    // w >= 120: at most one set per warp (set h); drain it in sub-batches of
-    // 12 groups (96 registers) with a running max
-    static_assert(EpiShape<W8>::MAXS == 1, "wide sets: one set per warp");
-    constexpr int G = 12;
-    constexpr int NS = (W8 + G - 1) / G;
-    const uint32_t c0 = taddr + (uint32_t)(h * w);
-    float mx = ninf;
+  }
+  if (mine <= 0) release();
+  // swap maxima: this warp finalises sets s = HH (mod 2)
 #pragma unroll
-    for (int sb = 0; sb < NS; ++sb) {
-      uint32_t r[G][8];
+  for (int s = 1 - HH; s < SPT; s += 2) xch[s * BM + row] = pm[s];
+  asm volatile("bar.sync %0, 64;" ::"r"(2 + q) : "memory");
 #pragma unroll
-      for (int g = 0; g < G; ++g)
-        if (sb * G + g < W8) TMEM_LD8(c0 + 8 * (sb * G + g), r[g]);
-      tmem_wait_ld();
-      if (sb == NS - 1) release();
-#pragma unroll
-      for (int g = 0; g < G; ++g)
-        if (sb * G + g < W8)
-          mx = kPlain ? max8b(r[g], bsm + h * w + 8 * (sb * G + g), mx)
-                      : max8(r[g], mx);
+  for (int u = 0; u < EpiShape<SPT>::OWN; ++u) {
+    const int s = HH + 2 * u;
+    if (s < SPT) {
+      const float mx = fmaxf(pm[s], xch[s * BM + row]);
+      // folded: min_e d = -2 max D;  plain: min_e d = a - 2 max (D - b)
+      const float dm = kPlain ? fmaf(-2.f, mx, ha) : -2.f * mx;
+      const float t = fminf(ax, fmaxf(0.f, dm));
+      if (valid) acc[u] += (double)t;
     }
-    const float dm = kPlain ? fmaf(-2.f, mx, ha) : -2.f * mx;
-    const float t = fminf(ax, fmaxf(0.f, dm));
-    if (valid) acc[0] += (double)t;
   }
 }
 
-// The epilogue warps' whole loop for one set width (W8 = w/8 at compile
-// time, so the per-set column runs and the accumulator array are static).
-// CG = 2: this CTA holds rows [128*rank, 128*rank+128) of each 256-point
-// pair tile; buffers are released on the leader's tempty, and at item end
-// the peer's per-set sums travel to the leader through DSMEM (xbuf) so the
-// leader writes one fixed-order partial per (split, set).
-template <int CG, int W8, bool kPlain>
+// The epilogue warps' whole loop for one sets-per-tile count (SPT at compile
+// time, so every column's set and the accumulator array are static) and one
+// group parity HH.  Work items follow the producer's order (item_of).
+template <int SPT, int HH, bool kPlain>
 __device__ __forceinline__ void epilogue_role(const BParams &p, uint32_t tmem,
                                               uint64_t *tfull,
                                               uint64_t *tempty, double *red,
-                                              double *xbuf, float *bsm,
-                                              uint64_t *xfull,
-                                              uint64_t *xempty, int warp,
-                                              int lane, int64_t items,
-                                              uint32_t rank, int64_t pair,
-                                              int64_t npairs) {
-  constexpr int MAXS = EpiShape<W8>::MAXS;
+                                              float *bsm, float *xch, int warp,
+                                              int lane, const WorkSplit &ws) {
+  constexpr int OWN = EpiShape<SPT>::OWN;
   const int ew = warp - 2;       // 0..7
   const int q = warp & 3;        // TMEM lane quarter (lane access rule)
-  const int h = ew >> 2;         // set parity handled by this warp
-  const int row = q * 32 + lane; // point row within this CTA's tile half
-  uint32_t buf = 0, tph = 0, xph = 0;
+  const int row = q * 32 + lane; // point row within the tile
+  const int ngroups = p.ncols >> 3;
+  uint32_t buf = 0, tph = 0;
 #ifdef EXEM_TCB_TRACE_BUILD
   int etile = 0;
   const bool tr = warp == 2 && lane == 0;
 #endif
-  for (int64_t it = pair; it < items; it += npairs) {
-    const int64_t st = it % p.set_tiles, sp = it / p.set_tiles;
+  for (int64_t u = ws.first; u < ws.units; u += ws.step) {
+    int64_t st, sp;
+    ws.item(u, st, sp);
     const int64_t p0 = sp * p.split_pts;
     const int64_t p1 = min(p.n, p0 + p.split_pts);
-    double acc[MAXS];
+    double acc[OWN];
 #pragma unroll
-    for (int u = 0; u < MAXS; ++u) acc[u] = 0.0;
+    for (int k = 0; k < OWN; ++k) acc[k] = 0.0;
     if constexpr (kPlain) {  // the set tile's column constants, once per item
       for (int c = ew * 32 + lane; c < p.ncols; c += kEpiWarps * 32)
-        bsm[c] = p.bs[st * p.ncols + c];
+        bsm[c] = st < p.set_tiles ? p.bs[st * p.ncols + c] : 0.f;
       asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
     }
-    for (int64_t pt = p0; pt < p1; pt += BM * CG) {
-      const int64_t pi = pt + BM * rank + row;
+    for (int64_t pt = p0; pt < p1; pt += BM) {
+      const int64_t pi = pt + row;
       const bool valid = pi < p1;
       const float ax = (valid && !(p.dbg & 8)) ? p.aux[pi] : 0.f;
       const float ha = (kPlain && valid) ? (float)p.norms[pi] : 0.f;
@@ -271,14 +238,33 @@ __device__ __forceinline__ void epilogue_role(const BParams &p, uint32_t tmem,
 #endif
       tph ^= 1u << buf;
       fence_after();
+#ifdef EXEM_TCB_TRACE_BUILD
+      if (tr) TRB(12, etile);
+#endif
       const uint32_t taddr =
           tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * 256);
-      TmemRelease<CG> rel{&tempty[buf], lane};
-      if (p.dbg & 1)  // timing experiment: no TMEM drain / math
+      TmemRelease rel{&tempty[buf], lane};
+      if (p.dbg & 1) {  // timing experiment: no TMEM drain / math
         rel();
-      else
-        epi_tile<W8, kPlain>(taddr, h, p.spt, p.w, ax, ha, valid, bsm, acc,
-                             rel);
+      } else {
+#ifdef EXEM_TCB_TRACE_BUILD
+        struct Traced {  // release + timestamp (slot 13)
+          TmemRelease r;
+          const BParams &p;
+          bool tr;
+          int etile;
+          __device__ void operator()() const {
+            r();
+            if (tr) TRB(13, etile);
+          }
+        } trel{rel, p, tr, etile};
+        epi_tile<SPT, HH, kPlain>(taddr, ngroups, q, row, ax, ha, valid, bsm,
+                                  xch + buf * (kMaxSpt * BM), acc, trel);
+#else
+        epi_tile<SPT, HH, kPlain>(taddr, ngroups, q, row, ax, ha, valid, bsm,
+                                  xch + buf * (kMaxSpt * BM), acc, rel);
+#endif
+      }
 #ifdef EXEM_TCB_TRACE_BUILD
       if (tr) TRB(4, etile);
       ++etile;
@@ -286,12 +272,12 @@ __device__ __forceinline__ void epilogue_role(const BParams &p, uint32_t tmem,
       buf ^= 1u;
     }
     // item end: per set, fixed xor tree over the 32 lanes, then the four
-    // lane quarters in order (then the pair's two CTAs in order)
+    // lane quarters in order
 #pragma unroll
-    for (int u = 0; u < MAXS; ++u) {
-      const int s = h + 2 * u;
-      if (s < p.spt) {
-        double v = acc[u];
+    for (int k = 0; k < OWN; ++k) {
+      const int s = HH + 2 * k;
+      if (s < SPT) {
+        double v = acc[k];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
         if (lane == 0) red[q * kMaxSpt + s] = v;
@@ -299,35 +285,11 @@ __device__ __forceinline__ void epilogue_role(const BParams &p, uint32_t tmem,
     }
     asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
     if (ew == 0) {
-      const bool mine = lane < p.spt;
-      const double tot =
-          mine ? ((red[lane] + red[kMaxSpt + lane]) + red[2 * kMaxSpt + lane]) +
-                     red[3 * kMaxSpt + lane]
-               : 0.0;
-      const int64_t j = st * p.spt + lane;
-      if constexpr (CG == 1) {
-        if (mine && j < p.l) p.partial[sp * p.l + j] = tot;
-      } else if (rank == 1) {
-        if (lane == 0) mbar_wait_cluster(xempty, xph ^ 1u);
-        __syncwarp();
-        if (mine) {
-          asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(
-                           mapa(&xbuf[lane], 0)),
-                       "d"(tot)
-                       : "memory");
-          asm volatile("fence.acq_rel.cluster;" ::: "memory");
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(mapa(xfull, 0));
-      } else {
-        if (lane == 0) mbar_wait_cluster(xfull, xph);
-        __syncwarp();
-        if (mine && j < p.l) p.partial[sp * p.l + j] = tot + xbuf[lane];
-        asm volatile("fence.acq_rel.cluster;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(mapa(xempty, 1));
-      }
-      xph ^= 1u;
+      const int64_t j = st * SPT + lane;  // >= l for a cluster's spare tile
+      if (lane < SPT && j < p.l)
+        p.partial[sp * p.l + j] =
+            ((red[lane] + red[kMaxSpt + lane]) + red[2 * kMaxSpt + lane]) +
+            red[3 * kMaxSpt + lane];
     }
     asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
   }
@@ -338,7 +300,10 @@ __device__ __forceinline__ void epilogue_role(const BParams &p, uint32_t tmem,
 // cycles of mbarrier latency each, profiles/r01_k4_probe.log): KS K-steps
 // unrolled at compile time, the next tile's point stage (full) acquired
 // before MMA KS-2 and its accumulator buffer (tempty) before MMA KS-1.
-template <int KS>
+template <int MC>
+__device__ __forceinline__ void release_stage(uint64_t *bar);
+
+template <int KS, int MC, bool kLate>
 __device__ __forceinline__ void k4_item_tstage(
     const BParams &p, int ntiles, int &stage, uint32_t &ph, uint32_t &tph,
     uint32_t &buf, int &itile, uint64_t a_base, uint32_t a_step,
@@ -347,8 +312,10 @@ __device__ __forceinline__ void k4_item_tstage(
   constexpr int WF = KS > 2 ? KS - 2 : 0;
   constexpr int WT = KS > 1 ? KS - 1 : 0;
   mbar_wait(&tempty[buf], ((tph >> buf) & 1u) ^ 1u);
+  TRB(0, itile);
   tph ^= 1u << buf;
   mbar_wait(&full[stage], ph);
+  TRB(1, itile);
   fence_after();
   for (int t = 0; t < ntiles; ++t) {
     const uint32_t d = tmem + buf * 256u;
@@ -365,10 +332,12 @@ __device__ __forceinline__ void k4_item_tstage(
     for (int ks = 0; ks < KS; ++ks) {
       if (ks == WF && more) {
         mbar_wait(&full[nstage], nph);
+        TRB(1, itile + 1);
         fence_after();
       }
-      if (ks == WT && more) {
+      if (!kLate && ks == WT && more) {
         mbar_wait(&tempty[nbuf], ((tph >> nbuf) & 1u) ^ 1u);
+        TRB(0, itile + 1);
         tph ^= 1u << nbuf;
         fence_after();
       }
@@ -377,9 +346,18 @@ __device__ __forceinline__ void k4_item_tstage(
                  b_base + (uint64_t)((ks >> 2) * b_step + (ks & 3) * 2),
                  p.idesc, ks > 0 ? 1u : 0u);
     }
-    umma_commit(&empty[stage]);
+    release_stage<MC>(&empty[stage]);
     umma_commit(&tfull[buf]);
     TRB(2, itile);
+    if (kLate && more) {
+      // the next buffer is acquired only after this tile's commit, so the
+      // commit (and the epilogue of this tile) never waits for the release
+      // of the previous tile -- the epilogue-bound shapes' critical chain
+      mbar_wait(&tempty[nbuf], ((tph >> nbuf) & 1u) ^ 1u);
+      TRB(0, itile + 1);
+      tph ^= 1u << nbuf;
+      fence_after();
+    }
     ++itile;
     buf = nbuf;
     stage = nstage;
@@ -389,20 +367,28 @@ __device__ __forceinline__ void k4_item_tstage(
 
 // MMA j of an event whose stage holds consecutive 64-wide K chunks: chunk
 // j>>2 of the event, K=16 step j&3 inside the 128-B swizzle row.
-template <int CG>
 __device__ __forceinline__ void issue_mma(const BParams &p, uint32_t d,
                                           uint64_t ad, uint64_t bd,
                                           uint32_t b_step, int kc, int j) {
   if (p.dbg & 2) return;  // timing experiment: no MMA
   const uint64_t a = ad + (uint64_t)((j >> 2) * (A_CHUNK >> 4) + (j & 3) * 2);
   const uint64_t b = bd + (uint64_t)((j >> 2) * b_step + (j & 3) * 2);
-  if constexpr (CG == 2)
-    umma_f16_pair(d, a, b, p.idesc, (kc | j) ? 1u : 0u);
-  else
-    umma_f16(d, a, b, p.idesc, (kc | j) ? 1u : 0u);
+  umma_f16(d, a, b, p.idesc, (kc | j) ? 1u : 0u);
 }
 
-template <int CG>
+// Release a point stage: on this CTA's empty barrier, or (MC > 1) on every
+// cluster CTA's -- their producers multicast into this CTA's copy.
+template <int MC>
+__device__ __forceinline__ void release_stage(uint64_t *bar) {
+  if constexpr (MC > 1)
+    umma_commit_mc(bar, (uint16_t)((1u << MC) - 1));
+  else
+    umma_commit(bar);
+}
+
+// MC: CTAs per cluster sharing every point tile by TMA multicast (1 = none).
+// map_p: the point operand with BM/MC-row boxes.
+template <int MC>
 __global__ void __launch_bounds__(kThreads, 1)
     batch_tc_kernel(const __grid_constant__ CUtensorMap map_p,
                     const __grid_constant__ CUtensorMap map_s,
@@ -410,8 +396,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char *smem = (unsigned char *)(((uintptr_t)smem_raw + 1023) &
                                           ~(uintptr_t)1023);
-  const int bh = p.ncols / CG;        // set-tile rows held by this CTA
-  const int b_chunk = bh * 128;       // bytes of one set-tile K-chunk half
+  const int b_chunk = p.ncols * 128;  // bytes of one set-tile K-chunk
   const int sb_bytes = p.bstream ? 0 : p.kchunks * b_chunk;
   const int stage_bytes = p.tstage ? p.kchunks * A_CHUNK
                                    : p.gch * A_CHUNK + (p.bstream ? b_chunk : 0);
@@ -424,123 +409,93 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t *tempty = tfull + 2;                    // [2]
   uint64_t *bfull = tempty + 2;                    // [1]
   uint64_t *bempty = bfull + 1;                    // [1]
-  uint64_t *xfull = bempty + 1;                    // [1] pair exchange (CTA 0)
-  uint64_t *xempty = xfull + 1;                    // [1] pair exchange (CTA 1)
-  uint32_t *tmem_slot = (uint32_t *)(xempty + 1);
+  uint32_t *tmem_slot = (uint32_t *)(bempty + 1);
   double *red = (double *)(tmem_slot + 4);         // [4][kMaxSpt]
-  double *xbuf = red + 4 * kMaxSpt;                // [kMaxSpt]
-  float *bsm = (float *)(xbuf + kMaxSpt);          // [256] plain: set b
+  float *bsm = (float *)(red + 4 * kMaxSpt);       // [256] plain: set b
+  float *xch = bsm + 256;                          // [2][kMaxSpt][BM]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = CG == 2 ? cluster_rank() : 0u;
-  const int64_t pair = blockIdx.x / CG, npairs = gridDim.x / CG;
+  WorkSplit ws;
+  ws.mc = MC;
+  ws.rank = MC > 1 ? cluster_rank() : 0u;
+  ws.groups = (p.set_tiles + MC - 1) / MC;
+  ws.units = ws.groups * p.splits;
+  ws.first = blockIdx.x / MC;
+  ws.step = gridDim.x / MC;
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < p.stages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], MC);  // one commit per cluster CTA
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], kEpiWarps * CG);
+      mbar_init(&tempty[b], kEpiWarps);
     }
     mbar_init(bfull, 1);
     mbar_init(bempty, 1);
-    mbar_init(xfull, 1);
-    mbar_init(xempty, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&map_p));
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&map_s));
   }
   if (warp == 1) {
-    if constexpr (CG == 2) {
-      asm volatile(
-          "tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::
-              "r"(su32(tmem_slot)));
-      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
-    } else {
-      asm volatile(
-          "tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::
-              "r"(su32(tmem_slot)));
-      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
+    asm volatile(
+        "tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::
+            "r"(su32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   fence_before();
   __syncthreads();
-  if constexpr (CG == 2) cluster_sync();
+  if constexpr (MC > 1) cluster_sync();  // peers' barriers initialised
   fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int64_t items = p.set_tiles * p.splits;
 
   if (warp == 0) {
     // -------------------------------------------------------------- producer
-    // Each CTA loads its own point rows and its half of the set tile; the
-    // completions are counted on the leader's barriers (CG = 2).
     if (lane == 0) {
       int stage = 0, ptile = 0;
       uint32_t ph = 0, bph = 0;
-      const uint32_t bfull_c = CG == 2 ? mapa(bfull, 0) : 0u;
-      for (int64_t it = pair; it < items; it += npairs) {
-        const int64_t st = it % p.set_tiles, sp = it / p.set_tiles;
-        const int srow = (int)(st * p.ncols) + (int)rank * bh;
+      const uint16_t mask = (uint16_t)((1u << MC) - 1);
+      const int prow_off = (int)ws.rank * (BM / MC);   // this CTA's rows
+      const int pdst_off = (int)ws.rank * (A_CHUNK / MC);
+      for (int64_t u = ws.first; u < ws.units; u += ws.step) {
+        int64_t st, sp;
+        ws.item(u, st, sp);
+        // a cluster's spare tile (st >= set_tiles) re-reads tile 0: valid
+        // memory, results never written
+        const int srow = st < p.set_tiles ? (int)(st * p.ncols) : 0;
         if (!p.bstream) {
           mbar_wait_sleep(bempty, bph ^ 1);
           bph ^= 1;
-          if (rank == 0) mbar_expect_tx(bfull, (uint32_t)(CG * sb_bytes));
-          for (int kc = 0; kc < p.kchunks; ++kc) {
-            if constexpr (CG == 2)
-              tma_load_2d_pair(sb + kc * b_chunk, &map_s, bfull_c, kc * KCH, srow);
-            else
-              tma_load_2d(sb + kc * b_chunk, &map_s, bfull, kc * KCH, srow);
-          }
+          mbar_expect_tx(bfull, (uint32_t)sb_bytes);
+          for (int kc = 0; kc < p.kchunks; ++kc)
+            tma_load_2d(sb + kc * b_chunk, &map_s, bfull, kc * KCH, srow);
         }
         const int64_t p0 = sp * p.split_pts;
         const int64_t p1 = min(p.n, p0 + p.split_pts);
-        for (int64_t pt = p0; pt < p1 && p.tstage; pt += BM, ++ptile) {
-          mbar_wait(&empty[stage], ph ^ 1);
-          TRB(5, ptile);
-          unsigned char *dst = sa + stage * stage_bytes;
-          if (p.dbg & 4) {
-            mbar_arrive(&full[stage]);
-          } else {
-            mbar_expect_tx(&full[stage], (uint32_t)stage_bytes);
-            for (int kc = 0; kc < p.kchunks; ++kc)
-              tma_load_2d(dst + kc * A_CHUNK, &map_p, &full[stage], kc * KCH,
-                          (int)pt);
-          }
-          TRB(6, ptile);
-          if (++stage == p.stages) {
-            stage = 0;
-            ph ^= 1;
-          }
-        }
-        for (int64_t pt = p0; pt < p1 && !p.tstage; pt += BM * CG, ++ptile) {
-          const int prow = (int)(pt + BM * rank);
-          for (int kc = 0; kc < p.kchunks; kc += p.gch) {
-            const int gn = p.kchunks - kc < p.gch ? p.kchunks - kc : p.gch;
-            mbar_wait_sleep(&empty[stage], ph ^ 1);
+        for (int64_t pt = p0; pt < p1; pt += BM, ++ptile) {
+          const int ng = p.tstage ? p.kchunks : p.gch;  // chunks per stage
+          for (int kc = 0; kc < p.kchunks; kc += ng) {
+            const int gn = p.kchunks - kc < ng ? p.kchunks - kc : ng;
+            mbar_wait(&empty[stage], ph ^ 1);
             if (kc == 0) TRB(5, ptile);
             unsigned char *dst = sa + stage * stage_bytes;
             if (p.dbg & 4) {  // timing experiment: no point-operand traffic
-              if (rank == 0) mbar_arrive(&full[stage]);
+              mbar_arrive(&full[stage]);
             } else {
-              const uint32_t bytes =
-                  (uint32_t)(gn * A_CHUNK + (p.bstream ? b_chunk : 0));
-              if (rank == 0) mbar_expect_tx(&full[stage], (uint32_t)CG * bytes);
-              if constexpr (CG == 2) {
-                const uint32_t fc = mapa(&full[stage], 0);
-                for (int j = 0; j < gn; ++j)
-                  tma_load_2d_pair(dst + j * A_CHUNK, &map_p, fc,
-                                   (kc + j) * KCH, prow);
-                if (p.bstream)
-                  tma_load_2d_pair(dst + A_CHUNK, &map_s, fc, kc * KCH, srow);
-              } else {
-                for (int j = 0; j < gn; ++j)
+              mbar_expect_tx(&full[stage],
+                             (uint32_t)(gn * A_CHUNK + (p.bstream ? b_chunk : 0)));
+              for (int j = 0; j < gn; ++j) {
+                if constexpr (MC > 1)
+                  tma_load_2d_mc(dst + j * A_CHUNK + pdst_off, &map_p,
+                                 &full[stage], (kc + j) * KCH,
+                                 (int)pt + prow_off, mask);
+                else
                   tma_load_2d(dst + j * A_CHUNK, &map_p, &full[stage],
-                              (kc + j) * KCH, prow);
-                if (p.bstream)
-                  tma_load_2d(dst + A_CHUNK, &map_s, &full[stage], kc * KCH,
-                              srow);
+                              (kc + j) * KCH, (int)pt);
               }
+              if (p.bstream)
+                tma_load_2d(dst + A_CHUNK, &map_s, &full[stage], kc * KCH,
+                            srow);
             }
             if (kc + gn >= p.kchunks) TRB(6, ptile);
             if (++stage == p.stages) {
@@ -553,41 +508,45 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    // (the leader CTA's single thread issues for the pair)
-    if (lane == 0 && rank == 0) {
+    if (lane == 0) {
       const uint64_t a_base = sw128_desc(su32(sa));
       const uint64_t b_base = sw128_desc(su32(sb));
       const uint32_t a_step = (uint32_t)(stage_bytes >> 4);
       const uint32_t b_step = (uint32_t)(b_chunk >> 4);
       int stage = 0, itile = 0;
       uint32_t ph = 0, bph = 0, tph = 0, buf = 0;
-      for (int64_t it = pair; it < items; it += npairs) {
-        const int64_t sp = it / p.set_tiles;
+      for (int64_t u = ws.first; u < ws.units; u += ws.step) {
+        int64_t st, sp;
+        ws.item(u, st, sp);
         const int64_t p0 = sp * p.split_pts;
         const int64_t p1 = min(p.n, p0 + p.split_pts);
-        const int ntiles = (int)((p1 - p0 + BM * CG - 1) / (BM * CG));
+        const int ntiles = (int)((p1 - p0 + BM - 1) / BM);
         const int kev = (p.kchunks + p.gch - 1) / p.gch;  // events per tile
         const int nev = ntiles * kev;
         if (!p.bstream) {
           mbar_wait(bfull, bph);
           bph ^= 1;
         }
-        if constexpr (CG == 1) {
-          if (p.tstage) {
-            switch (p.ksteps) {
+        if (p.tstage) {
+          switch (p.ksteps) {
 #define EXEM_K4_ITEM(K)                                                       \
   case K:                                                                     \
-    k4_item_tstage<K>(p, ntiles, stage, ph, tph, buf, itile, a_base, a_step, \
-                      b_base, b_step, tmem, full, empty, tfull, tempty);      \
+    if (p.late)                                                               \
+      k4_item_tstage<K, MC, true>(p, ntiles, stage, ph, tph, buf, itile,      \
+                                  a_base, a_step, b_base, b_step, tmem, full, \
+                                  empty, tfull, tempty);                      \
+    else                                                                      \
+      k4_item_tstage<K, MC, false>(p, ntiles, stage, ph, tph, buf, itile,     \
+                                   a_base, a_step, b_base, b_step, tmem,      \
+                                   full, empty, tfull, tempty);               \
     break;
-              EXEM_K4_ITEM(1) EXEM_K4_ITEM(2) EXEM_K4_ITEM(3) EXEM_K4_ITEM(4)
-              EXEM_K4_ITEM(5) EXEM_K4_ITEM(6) EXEM_K4_ITEM(7)
-              default: EXEM_K4_ITEM(8)
+            EXEM_K4_ITEM(1) EXEM_K4_ITEM(2) EXEM_K4_ITEM(3) EXEM_K4_ITEM(4)
+            EXEM_K4_ITEM(5) EXEM_K4_ITEM(6) EXEM_K4_ITEM(7)
+            default: EXEM_K4_ITEM(8)
 #undef EXEM_K4_ITEM
-            }
-            umma_commit(bempty);
-            continue;
           }
+          umma_commit(bempty);
+          continue;
         }
         // acquire event 0 (accumulator buffer free + point chunk landed)
         mbar_wait(&tempty[buf], ((tph >> buf) & 1u) ^ 1u);
@@ -620,11 +579,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           const bool trc = kc == 1 || (p.kchunks == 1);
           if (trc) TRB(7, itile);
 #pragma unroll 1
-          for (int j = 0; j < head; ++j)
-            issue_mma<CG>(p, d, ad, bd, b_step, kc, j);
+          for (int j = 0; j < head; ++j) issue_mma(p, d, ad, bd, b_step, kc, j);
           if (trc) TRB(8, itile);
           if (e + 1 < nev) {
-            if (last) {
+            if (last && !p.late) {
               const uint32_t nb = buf ^ 1u;
               mbar_wait(&tempty[nb], ((tph >> nb) & 1u) ^ 1u);
               TRB(0, itile + 1);
@@ -638,16 +596,20 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           if (trc) TRB(9, itile);
 #pragma unroll 1
-          for (int j = head; j < nk; ++j)
-            issue_mma<CG>(p, d, ad, bd, b_step, kc, j);
+          for (int j = head; j < nk; ++j) issue_mma(p, d, ad, bd, b_step, kc, j);
           if (trc) TRB(10, itile);
-          if constexpr (CG == 2) umma_commit_pair(&empty[stage]);
-          else umma_commit(&empty[stage]);
+          release_stage<MC>(&empty[stage]);
           if (trc) TRB(11, itile);
           if (last) {
-            if constexpr (CG == 2) umma_commit_pair(&tfull[buf]);
-            else umma_commit(&tfull[buf]);
+            umma_commit(&tfull[buf]);
             TRB(2, itile);
+            if (p.late && e + 1 < nev) {  // see k4_item_tstage<.., kLate>
+              const uint32_t nb = buf ^ 1u;
+              mbar_wait(&tempty[nb], ((tph >> nb) & 1u) ^ 1u);
+              TRB(0, itile + 1);
+              tph ^= 1u << nb;
+              fence_after();
+            }
             ++itile;
             buf ^= 1u;
             kc = 0;
@@ -657,60 +619,52 @@ __global__ void __launch_bounds__(kThreads, 1)
           stage = nstage;
           ph = nph;
         }
-        if (!p.bstream) {
-          if constexpr (CG == 2) umma_commit_pair(bempty);
-          else umma_commit(bempty);
-        }
+        if (!p.bstream) umma_commit(bempty);
       }
     }
     __syncwarp();
   } else {
     // -------------------------------------------------------------- epilogue
-    switch (p.w >> 3) {
-#define EXEM_EPI_CASE(W)                                                     \
-  case W:                                                                    \
-    if (p.plain)                                                             \
-      epilogue_role<CG, W, true>(p, tmem, tfull, tempty, red, xbuf, bsm,     \
-                                 xfull, xempty, warp, lane, items, rank,     \
-                                 pair, npairs);                              \
-    else                                                                     \
-      epilogue_role<CG, W, false>(p, tmem, tfull, tempty, red, xbuf, bsm,    \
-                                  xfull, xempty, warp, lane, items, rank,    \
-                                  pair, npairs);                             \
+    const bool hh = (warp - 2) >= 4;  // 8-column group parity of this warp
+    switch (p.spt) {
+#define EXEM_EPI_ROLE(S, H, PL) \
+  epilogue_role<S, H, PL>(p, tmem, tfull, tempty, red, bsm, xch, warp, lane, ws)
+#define EXEM_EPI_CASE(S)                                                     \
+  case S:                                                                    \
+    if (p.plain) {                                                           \
+      if (hh) EXEM_EPI_ROLE(S, 1, true); else EXEM_EPI_ROLE(S, 0, true);     \
+    } else {                                                                 \
+      if (hh) EXEM_EPI_ROLE(S, 1, false); else EXEM_EPI_ROLE(S, 0, false);   \
+    }                                                                        \
     break;
       EXEM_EPI_CASE(1) EXEM_EPI_CASE(2) EXEM_EPI_CASE(3) EXEM_EPI_CASE(4)
       EXEM_EPI_CASE(5) EXEM_EPI_CASE(6) EXEM_EPI_CASE(7) EXEM_EPI_CASE(8)
       EXEM_EPI_CASE(9) EXEM_EPI_CASE(10) EXEM_EPI_CASE(11) EXEM_EPI_CASE(12)
       EXEM_EPI_CASE(13) EXEM_EPI_CASE(14) EXEM_EPI_CASE(15) EXEM_EPI_CASE(16)
-      EXEM_EPI_CASE(17) EXEM_EPI_CASE(18) EXEM_EPI_CASE(19) EXEM_EPI_CASE(20)
-      EXEM_EPI_CASE(21) EXEM_EPI_CASE(22) EXEM_EPI_CASE(23) EXEM_EPI_CASE(24)
-      EXEM_EPI_CASE(25) EXEM_EPI_CASE(26) EXEM_EPI_CASE(27) EXEM_EPI_CASE(28)
-      EXEM_EPI_CASE(29) EXEM_EPI_CASE(30) EXEM_EPI_CASE(31) EXEM_EPI_CASE(32)
 #undef EXEM_EPI_CASE
+#undef EXEM_EPI_ROLE
       default: break;
     }
   }
 
   fence_before();
   __syncthreads();
-  if constexpr (CG == 2) cluster_sync();
+  if constexpr (MC > 1) cluster_sync();  // no multicast / commit in flight
   if (warp == 1) {
     fence_after();
-    if constexpr (CG == 2)
-      asm volatile(
-          "tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
-    else
-      asm volatile(
-          "tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    asm volatile(
+        "tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
 }
 
 // ---------------------------------------------------------------- packing
 // Set-tile operand rows from the packed round-robin batch
 // packed[d_pad][k_max][l_pad] (compute type, packed_address order,
-// core.py:320-328).  Row r = tile*ncols + s*w + e holds element
-// (e < card_j ? e : 0) of set j = tile*spt + s, then the folded constants;
-// rows of sets j >= l and padding columns past spt*w are zero.
+// core.py:320-328).  Column-interleaved like the packed batch itself: row
+// r = tile*ncols + c holds slot e = c / spt of set j = tile*spt + c % spt --
+// element (e < card_j ? e : 0), then the folded constants -- so blank slots
+// and the padding columns past spt*k_max repeat the set's element 0 (never
+// change a minimum, need no mask).  Rows of sets j >= l are zero.
 template <int DT>
 __global__ void pack_sets_kernel(const float *__restrict__ packed,
                                  const double *__restrict__ pnorms,
@@ -724,9 +678,9 @@ __global__ void pack_sets_kernel(const float *__restrict__ packed,
   if (r >= rows) return;
   const int64_t tile = r / ncols;
   const int c = (int)(r % ncols);
-  const int s = c / w, e = c % w;
+  const int s = c % spt, e = c / spt;
   const int64_t j = tile * spt + s;
-  const bool real = s < spt && j < l;
+  const bool real = j < l;
   const int src = real ? (e < card[j] ? e : 0) : 0;
   const int64_t ldp = (int64_t)k_max * l_pad;
   if (bs != nullptr && threadIdx.x == 0)  // plain: the column's b = ||e||^2/2
@@ -774,6 +728,45 @@ __global__ void pack_plain_kernel(const float *__restrict__ vt, int64_t ld,
   }
 }
 
+// Launch one persistent CTA per SM (clusters of MC), at most one per unit.
+template <int MC>
+cudaError_t launch_batch(const BParams &prm, const CUtensorMap &mp,
+                         const CUtensorMap &ms, size_t smem, int sms,
+                         int64_t splits, void *stream) {
+  cudaError_t e = cudaFuncSetAttribute(
+      batch_tc_kernel<MC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      (int)smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = (cudaStream_t)stream;
+  const int64_t units = (prm.set_tiles + MC - 1) / MC * splits;
+  int64_t clusters = sms / MC;
+  if (MC > 1) {
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = MC;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cfg.gridDim = dim3((unsigned)(clusters * MC));
+    int active = 0;
+    e = cudaOccupancyMaxActiveClusters(&active, batch_tc_kernel<MC>, &cfg);
+    if (e != cudaSuccess) return e;
+    if (active < 1) return cudaErrorLaunchOutOfResources;
+    if (active < clusters) clusters = active;
+  }
+  if (units < clusters) clusters = units;
+  cfg.gridDim = dim3((unsigned)(clusters * MC));
+  if (getenv("EXEM_TCB_VERBOSE"))
+    fprintf(stderr, "batch_tc<%d>: grid=%u stages=%d smem=%zu bstream=%d "
+            "tstage=%d gch=%d\n", MC, cfg.gridDim.x, prm.stages, smem,
+            prm.bstream, prm.tstage, prm.gch);
+  return cudaLaunchKernelEx(&cfg, batch_tc_kernel<MC>, mp, ms, prm);
+}
+
 }  // namespace tcb
 }  // namespace exem
 
@@ -784,7 +777,7 @@ extern "C" {
 int exem_tc_set_geometry(int64_t k_max, int32_t *spt, int32_t *w,
                          int32_t *ncols) {
   if (k_max < 1) return fail(EXEM_ERR_ARG, "k_max must be >= 1");
-  const int64_t ww = round_up(k_max, 8);
+  const int64_t ww = k_max;  // slots per set (interleaved, no padding)
   if (ww > 256)
     return fail(EXEM_ERR_UNSUPPORTED,
                 "tcgen05 batch path holds a set in <= 256 TMEM columns "
@@ -900,15 +893,15 @@ int exem_batch_eval_tc(int dtype, const void *xp, int64_t n, const void *aux,
   prm.ncols = nc;
   prm.ksteps = (int)ceil_div(d + (plain ? 0 : kTcConst), 16);
   prm.kchunks = (int)(kp / KCH);
-  // Single-CTA tiles by default.  EXEM_TCB_CG=2 selects CTA pairs
-  // (cta_group::2, M = 256, each CTA holding half of the set tile, 9 instead
-  // of 5 point-chunk stages at d = 256): correct (tests) but measured no
-  // faster at d = 256 and 1.4x slower at d = 100 (tools/k4_cg_compare.sh,
-  // profiles/r01_k4_probe.log) -- the per-chunk cross-SM handshake costs
-  // more than the deeper ring saves.
-  int cg = 1;
-  if (const char *e = getenv("EXEM_TCB_CG")) cg = atoi(e) == 2 ? 2 : 1;
-  prm.idesc = make_idesc(dtype == EXEM_BF16, BM * cg, nc);
+  prm.idesc = make_idesc(dtype == EXEM_BF16, BM, nc);
+  // Acquire the next accumulator buffer after a tile's commit (instead of
+  // before its last MMA) when few, wide sets make the epilogue the longer
+  // leg: d = 100, 1M x 4096 sets, |S| = 50 / 64 / 100: 42.0 -> 39.3,
+  // 53.0 -> 48.7, 96.3 -> 88.1 ms; |S| <= 32 (spt >= 8) is slower that way
+  // and the chunked-stage layouts (d > 122) do not care
+  // (tools/k4_late.sh, profiles/r01_k4_probe.log).  EXEM_TCB_LATE overrides.
+  prm.late = spt <= 5 ? 1 : 0;
+  if (const char *e = getenv("EXEM_TCB_LATE")) prm.late = atoi(e) ? 1 : 0;
   prm.aux = (const float *)aux;
   {
     const char *dbg = getenv("EXEM_TCB_DEBUG");
@@ -918,17 +911,17 @@ int exem_batch_eval_tc(int dtype, const void *xp, int64_t n, const void *aux,
   prm.trace = nullptr;
   const char *trace_path = getenv("EXEM_TCB_TRACE");
   if (trace_path) {
-    cudaMalloc(&prm.trace, 12 * kTrace * sizeof(long long));
-    cudaMemset(prm.trace, 0, 12 * kTrace * sizeof(long long));
+    cudaMalloc(&prm.trace, 16 * kTrace * sizeof(long long));
+    cudaMemset(prm.trace, 0, 16 * kTrace * sizeof(long long));
   }
-  const int b_chunk = (nc / cg) * 128;
+  const int b_chunk = nc * 128;
   const int avail = kSmemBudget - kBarBytes - 1024;
   // set tile stationary when it leaves room for >= 3 point-chunk stages
   const bool bstream = (avail - prm.kchunks * b_chunk) / A_CHUNK < 3;
   const int sb_bytes = bstream ? 0 : prm.kchunks * b_chunk;
   // whole-tile point stages (one handshake per tile) when >= 3 fit and the
   // K loop unrolls (K <= 128); EXEM_TCB_DEBUG 128 disables (timing only)
-  const bool tstage = cg == 1 && !bstream && prm.ksteps <= 8 &&
+  const bool tstage = !bstream && prm.ksteps <= 8 &&
                       (avail - sb_bytes) / (prm.kchunks * A_CHUNK) >= 3 &&
                       !(prm.dbg & 128);
   prm.tstage = tstage ? 1 : 0;
@@ -949,64 +942,37 @@ int exem_batch_eval_tc(int dtype, const void *xp, int64_t n, const void *aux,
   prm.bstream = bstream ? 1 : 0;
   const size_t smem = (size_t)sb_bytes + (size_t)stages * stage_bytes +
                       kBarBytes + 1024;
+  // Point tiles shared by TMA multicast across clusters of MC CTAs scoring
+  // adjacent set tiles (default 2; EXEM_TCB_MC = 1, 2 or 4 for experiments).
+  // The streamed-set-tile layout keeps MC = 1.
+  int mc = 2;
+  if (const char *e = getenv("EXEM_TCB_MC")) {
+    const int f = atoi(e);
+    mc = (f == 1 || f == 4) ? f : 2;
+  }
+  if (bstream) mc = 1;
   CUtensorMap mp, ms;
-  if (int rc = make_map(&mp, xp, dtype, exem_tc_rows(n), kp, BM)) return rc;
-  if (int rc = make_map(&ms, xs, dtype, exem_tc_set_rows(l, k_max), kp,
-                        nc / cg))
+  if (int rc = make_map(&mp, xp, dtype, exem_tc_rows(n), kp, BM / mc)) return rc;
+  if (int rc = make_map(&ms, xs, dtype, exem_tc_set_rows(l, k_max), kp, nc))
     return rc;
-  const int64_t items = prm.set_tiles * splits;
-  cudaLaunchConfig_t cfg = {};
-  cudaLaunchAttribute at[1];
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = (cudaStream_t)stream;
   cudaError_t e;
-  if (cg == 2) {
-    e = cudaFuncSetAttribute(batch_tc_kernel<2>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-    if (e != cudaSuccess)
-      return fail(EXEM_ERR_CUDA, "smem attr: %s", cudaGetErrorString(e));
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    int clusters = 0;
-    cfg.gridDim = dim3((unsigned)(sms & ~1));
-    e = cudaOccupancyMaxActiveClusters(&clusters, batch_tc_kernel<2>, &cfg);
-    if (e != cudaSuccess || clusters < 1)
-      return fail(EXEM_ERR_CUDA, "no co-resident CTA pairs: %s",
-                  cudaGetErrorString(e));
-    const int64_t pairs = items < clusters ? items : clusters;
-    cfg.gridDim = dim3((unsigned)(2 * pairs));
-    if (getenv("EXEM_TCB_VERBOSE"))
-      fprintf(stderr, "batch_tc<2>: clusters=%d grid=%u stages=%d smem=%zu "
-              "bstream=%d\n", clusters, cfg.gridDim.x, stages, smem,
-              (int)bstream);
-    e = cudaLaunchKernelEx(&cfg, batch_tc_kernel<2>, mp, ms, prm);
-  } else {
-    e = cudaFuncSetAttribute(batch_tc_kernel<1>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-    if (e != cudaSuccess)
-      return fail(EXEM_ERR_CUDA, "smem attr: %s", cudaGetErrorString(e));
-    cfg.gridDim = dim3((unsigned)(items < sms ? items : sms));
-    e = cudaLaunchKernelEx(&cfg, batch_tc_kernel<1>, mp, ms, prm);
+  switch (mc) {
+    case 1: e = launch_batch<1>(prm, mp, ms, smem, sms, splits, stream); break;
+    case 4: e = launch_batch<4>(prm, mp, ms, smem, sms, splits, stream); break;
+    default: e = launch_batch<2>(prm, mp, ms, smem, sms, splits, stream); break;
   }
   if (e != cudaSuccess)
     return fail(EXEM_ERR_CUDA, "batch_tc_kernel launch: %s",
                 cudaGetErrorString(e));
   if (prm.trace) {  // timing experiment: dump the CTA-0 timeline
-    static long long host[12 * kTrace];
+    static long long host[16 * kTrace];
     cudaStreamSynchronize((cudaStream_t)stream);
     cudaMemcpy(host, prm.trace, sizeof(host), cudaMemcpyDeviceToHost);
     cudaFree(prm.trace);
     if (FILE *f = fopen(trace_path, "w")) {
       for (int t = 0; t < kTrace; ++t)
-        for (int s2 = 0; s2 < 12; ++s2)
-          fprintf(f, "%lld%c", host[s2 * kTrace + t], s2 == 11 ? '\n' : ' ');
+        for (int s2 = 0; s2 < 16; ++s2)
+          fprintf(f, "%lld%c", host[s2 * kTrace + t], s2 == 15 ? '\n' : ' ');
       fclose(f);
     }
   }

@@ -111,14 +111,19 @@ def test_tc_batch_large_sets_use_simt_path():
     _check(g, sets, vals)
 
 
-def test_tc_batch_cta_pair_variant(monkeypatch):
-    """The cta_group::2 variant of K4-TC (EXEM_TCB_CG=2: M = 256 over a CTA
-    pair, set tile split across the pair, per-set sums combined through
-    DSMEM) against the fp64 oracle and the single-CTA kernel."""
+@pytest.mark.parametrize("l", [1, 7, 23])
+def test_tc_batch_multicast_clusters_identical(monkeypatch, l):
+    """Point tiles shared by TMA multicast across clusters of 1, 2 or 4 CTAs
+    (EXEM_TCB_MC; default 2) give bit-identical sums -- every (split, set)
+    partial is still computed by one CTA in a fixed order -- including an odd
+    number of set tiles (a cluster's spare tile is computed and dropped)."""
     g, sets = _case(BF16, 9000, 100, 50, 1, 50, seed=17)
+    sets = (sets * 3)[:l * 5]
     batch = EvaluationBatch.from_sets([g.matrix[i] for i in sets])
-    one = pb.evaluate_batch(Evaluator(), g, batch)
-    monkeypatch.setenv("EXEM_TCB_CG", "2")
-    two = pb.evaluate_batch(Evaluator(), g, batch)
-    _check(g, sets, two, nref=20)
-    np.testing.assert_allclose(two, one, rtol=1e-6, atol=1e-6)
+    out = {}
+    for mc in ("1", "2", "4"):
+        monkeypatch.setenv("EXEM_TCB_MC", mc)
+        out[mc] = pb.evaluate_batch(Evaluator(), g, batch)
+    _check(g, sets, out["2"], nref=20)
+    assert np.array_equal(out["1"], out["2"])
+    assert np.array_equal(out["1"], out["4"])

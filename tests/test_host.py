@@ -284,17 +284,17 @@ def test_stream_plan_is_split_aligned(native_lib):
 
 
 def test_tc_set_geometry(native_lib):
-    """K4-TC set tiles: w = round_up(k_max, 8) columns per set, as many whole
-    sets as fit 256 TMEM columns (<= 16), MMA N a multiple of 16."""
+    """K4-TC set tiles: w = k_max slots per set (column-interleaved), as many
+    sets as fit 256 TMEM columns (<= 16), MMA N = round_up(spt*w, 16)."""
     import ctypes
 
     geo = native_lib.raw("exem_tc_set_geometry")
-    for k in (1, 7, 8, 9, 50, 128, 129, 256):
+    for k in (1, 7, 8, 9, 50, 51, 128, 129, 256):
         spt, w, nc = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
         assert geo(k, ctypes.byref(spt), ctypes.byref(w), ctypes.byref(nc)) == 0
-        assert w.value == -(-k // 8) * 8
-        assert spt.value == min(16, 256 // w.value)
-        assert nc.value % 16 == 0 and spt.value * w.value <= nc.value <= 256
+        assert w.value == k
+        assert spt.value == min(16, 256 // k)
+        assert nc.value == -(-spt.value * k // 16) * 16 <= 256
         rows = native_lib.tc_set_rows(1000, k)
         assert rows == -(-1000 // spt.value) * nc.value
     spt, w, nc = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
