@@ -79,11 +79,15 @@ int64_t exem_reduce_scratch(int64_t count);  /* doubles of scratch needed by
  *            dtype (the reference stores aux_distances at dt, core.py:304).
  *   aux_sum  out [1] double, sum_i aux_i in fixed order.
  *   scratch  exem_reduce_scratch(n) doubles.
+ *   check_finite  != 0 (f32/f16/bf16 storage): a point with a non-finite
+ *            stored value contributes NaN to the aux sum, so aux_sum is NaN
+ *            iff V holds inf/NaN -- the device-side replacement of the
+ *            reference's host scan (core.py:282-283).
  */
 int exem_ground_prepare(int dtype, const void *src, int64_t n, int64_t d,
                         const void *e0, void *vt, int64_t ld, double *norms,
                         void *aux, double *aux_sum, double *scratch,
-                        void *stream);
+                        int check_finite, void *stream);
 
 /*
  * Low-memory regime (north-star item c): V stays in (pinned) host memory and
@@ -113,7 +117,7 @@ int exem_sum_fixed(const double *in, int64_t count, double *out,
 int exem_ground_prepare_rows(int dtype, const void *src, int64_t n, int64_t d,
                              const void *e0, void *vt, int64_t ld,
                              double *norms, void *aux, double *aux_sum,
-                             double *scratch, void *stream);
+                             double *scratch, int check_finite, void *stream);
 /* Plain async host -> device copy (a contiguous row slice of a row-major
  * host matrix in the low-memory regime). */
 int exem_h2d_bytes(void *dst, const void *host, int64_t bytes, void *stream);

@@ -41,7 +41,7 @@ _SIGNATURES = {
     "exem_tc_rows": (c_int64, [c_int64]),
     "exem_reduce_scratch": (c_int64, [c_int64]),
     "exem_ground_prepare": (c_int, [c_int, _P, c_int64, c_int64, _P, _P,
-                                    c_int64, _P, _P, _P, _P, _P]),
+                                    c_int64, _P, _P, _P, _P, c_int, _P]),
     "exem_set_min": (c_int, [c_int, _P, c_int64, c_int64, c_int64, _P, _P, _P,
                              _P, c_int64, c_int, _P, _P, _P, _P, _P]),
     "exem_batch_eval": (c_int, [c_int, _P, c_int64, c_int64, c_int64, _P, _P,
@@ -103,7 +103,7 @@ _SIGNATURES = {
                                         c_int64, c_double, _P, _P, c_int64,
                                         _P, _P, _P, _P]),
     "exem_ground_prepare_rows": (c_int, [c_int, _P, c_int64, c_int64, _P, _P,
-                                         c_int64, _P, _P, _P, _P, _P]),
+                                         c_int64, _P, _P, _P, _P, c_int, _P]),
     "exem_h2d_bytes": (c_int, [_P, _P, c_int64, _P]),
     "exem_launch_count": (c_int64, []),
 }

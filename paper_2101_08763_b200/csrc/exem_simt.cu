@@ -60,6 +60,21 @@ static int reduce_fixed(const double *partials, int64_t count, double *out,
 }
 
 // ============================================================ K1 prepare
+// Non-finite stored values, detected on the device: for f32/f16/bf16 storage
+// ||v_i||^2 (accumulated in fp64, which cannot overflow for these widths) is
+// finite iff every coordinate is, so a non-finite norm turns the point's aux
+// term into NaN and the fixed-order aux sum is NaN iff some stored value is
+// inf/NaN (aux terms of finite points are never NaN).  The host raises
+// InvalidDataError on it instead of scanning V itself (core.py).  Binary64
+// storage keeps the host check (a finite 1e200 would overflow the norm).
+template <int DT>
+__device__ __forceinline__ double nonfinite_mark(bool mark, double nrm,
+                                                 double term) {
+  if (DT != EXEM_F64 && mark && !isfinite(nrm))
+    return __longlong_as_double(0x7ff8000000000000LL);
+  return term;
+}
+
 template <int DT>
 __global__ void __launch_bounds__(kRedThreads)
     ground_prepare_kernel(const typename Traits<DT>::S *__restrict__ src,
@@ -68,7 +83,7 @@ __global__ void __launch_bounds__(kRedThreads)
                           typename Traits<DT>::C *__restrict__ vt, int64_t ld,
                           double *__restrict__ norms,
                           typename Traits<DT>::C *__restrict__ aux,
-                          double *__restrict__ partials) {
+                          double *__restrict__ partials, bool mark) {
   using S = typename Traits<DT>::S;
   using C = typename Traits<DT>::C;
   __shared__ double sh[32];
@@ -97,7 +112,7 @@ __global__ void __launch_bounds__(kRedThreads)
       norms[i] = 0.0;
       aux[i] = C(0);
     }
-    dst = (i < n) ? (double)a : 0.0;
+    dst = (i < n) ? nonfinite_mark<DT>(mark, nrm, (double)a) : 0.0;
   }
   double r = block_sum<kRedThreads>(dst, sh);
   if (threadIdx.x == 0) partials[blockIdx.x] = r;
@@ -117,7 +132,7 @@ __global__ void __launch_bounds__(kRedThreads)
                                typename Traits<DT>::C *__restrict__ vt,
                                int64_t ld, double *__restrict__ norms,
                                typename Traits<DT>::C *__restrict__ aux,
-                               double *__restrict__ partials) {
+                               double *__restrict__ partials, bool mark) {
   using S = typename Traits<DT>::S;
   using C = typename Traits<DT>::C;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -159,7 +174,7 @@ __global__ void __launch_bounds__(kRedThreads)
       norms[i] = 0.0;
       aux[i] = C(0);
     }
-    dst = (i < n) ? (double)a : 0.0;
+    dst = (i < n) ? nonfinite_mark<DT>(mark, nrm, (double)a) : 0.0;
   } else {
     dst = 0.0;
   }
@@ -917,7 +932,7 @@ int64_t exem_reduce_scratch(int64_t count) {
 int exem_ground_prepare(int dtype, const void *src, int64_t n, int64_t d,
                         const void *e0, void *vt, int64_t ld, double *norms,
                         void *aux, double *aux_sum, double *scratch,
-                        void *stream) {
+                        int check_finite, void *stream) {
   if (n < 1 || d < 1 || ld < n || ld % kPointPad)
     return fail(EXEM_ERR_ARG, "ground_prepare: bad shape n=%lld d=%lld ld=%lld",
                 (long long)n, (long long)d, (long long)ld);
@@ -929,7 +944,7 @@ int exem_ground_prepare(int dtype, const void *src, int64_t n, int64_t d,
     using C = typename Traits<DT>::C;
     ground_prepare_kernel<DT><<<(unsigned)blocks, kRedThreads, 0, st>>>(
         (const S *)src, n, (int)d, d_pad, (const S *)e0, (C *)vt, ld, norms,
-        (C *)aux, scratch);
+        (C *)aux, scratch, check_finite != 0);
     EXEM_LAUNCH_CHECK("ground_prepare_kernel");
   });
   // aux_sum == NULL: leave the per-256-point block partials in scratch (a
@@ -1329,7 +1344,7 @@ int exem_peer_argmax_select(const double *const *peers,
 int exem_ground_prepare_rows(int dtype, const void *src, int64_t n, int64_t d,
                              const void *e0, void *vt, int64_t ld,
                              double *norms, void *aux, double *aux_sum,
-                             double *scratch, void *stream) {
+                             double *scratch, int check_finite, void *stream) {
   if (n < 1 || d < 1 || ld < n || ld % kPointPad)
     return fail(EXEM_ERR_ARG, "ground_prepare_rows: bad shape");
   cudaStream_t st = (cudaStream_t)stream;
@@ -1349,7 +1364,7 @@ int exem_ground_prepare_rows(int dtype, const void *src, int64_t n, int64_t d,
     }
     ground_prepare_rows_kernel<DT><<<(unsigned)blocks, kRedThreads, smem, st>>>(
         (const S *)src, n, (int)d, d_pad, (const S *)e0, (C *)vt, ld, norms,
-        (C *)aux, scratch);
+        (C *)aux, scratch, check_finite != 0);
     EXEM_LAUNCH_CHECK("ground_prepare_rows_kernel");
   });
   if (!aux_sum) return EXEM_OK;

@@ -178,7 +178,7 @@ def row_major(matrix: np.ndarray) -> bool:
 
 
 def prepare_ground(matrix: np.ndarray, aux_vec: np.ndarray, precision,
-                   device=None):
+                   device=None, check_finite: bool = False):
     """Upload V in its host layout and run K1 (column-major, the reference's
     layout, or row-major); return (state, aux_dist, sum)."""
     t = torch()
@@ -199,7 +199,7 @@ def prepare_ground(matrix: np.ndarray, aux_vec: np.ndarray, precision,
                    else lib.ground_prepare)
         prepare(precision.tag, N.ptr(src), n, d, N.ptr(e0), N.ptr(dg.vt),
                 dg.ld, N.ptr(dg.norms), N.ptr(dg.aux), N.ptr(dg.aux_sum),
-                N.ptr(dg.scratch), dg.stream)
+                N.ptr(dg.scratch), int(check_finite), dg.stream)
         aux_host = dg.aux[:n].cpu().numpy().astype(aux_dtype(precision))
         aux_sum = float(dg.aux_sum.item())
         del src, e0

@@ -199,6 +199,7 @@ class GroundStream:
 
         host = ground.matrix
         self.row_major = row_major(host)
+        self.check_finite = False  # set by stream_build (K1 NaN marker)
         assert self.row_major or host.flags.f_contiguous
         self._host_ptr = c_void_p(host.ctypes.data)
         with t.cuda.device(self.idx):
@@ -234,7 +235,7 @@ class GroundStream:
         fn = (self.lib.ground_prepare_rows if self.row_major
               else self.lib.ground_prepare)
         fn(self.prec.tag, src, rows, self.d, N.ptr(self.e0), vt, ld, norms,
-           aux, None, partials, stream)
+           aux, None, partials, int(self.check_finite), stream)
 
     def block_ptr(self, r0: int) -> c_void_p:
         return c_void_p(self.block_partials.data_ptr() + (r0 // 256) * 8)
@@ -276,12 +277,15 @@ class GroundStream:
 
 
 # ---------------------------------------------------------------- consumers
-def stream_build(ground, free_bytes: int, device=None):
-    """Streamed K1: (aux_distances host array, fixed-order aux sum)."""
+def stream_build(ground, free_bytes: int, device=None,
+                 check_finite: bool = False):
+    """Streamed K1: (aux_distances host array, fixed-order aux sum; NaN iff
+    ``check_finite`` and V holds a non-finite stored value)."""
     from .device import aux_dtype, torch
 
     t = torch()
     gs = GroundStream(ground, free_bytes - _margin(ground.n), device)
+    gs.check_finite = check_finite
     try:
         with t.cuda.device(gs.idx):
             cdt = t.float64 if ground.precision.compute_dtype == np.float64 \

@@ -159,3 +159,31 @@ def test_row_major_input_matches_column_major(prec):
             assert np.array_equal(got[2], ref[2])
             assert got[3].exemplar_indices == ref[3].exemplar_indices
             assert got[3].values == ref[3].values
+
+
+@pytest.mark.parametrize("prec", [P32, BF16])
+@pytest.mark.parametrize("streamed", [False, True])
+@pytest.mark.parametrize("bad", [np.nan, np.inf, -np.inf])
+def test_nonfinite_detected_on_device(prec, streamed, bad):
+    """binary32 storage of a float32 matrix and bfloat16 storage skip the
+    host scan: K1 turns a non-finite stored value into a NaN aux sum and
+    build_ground_set raises the reference's InvalidDataError (core.py:282-283)
+    -- wherever the value sits (first / last point, a late streamed slice)."""
+    rng = np.random.default_rng(2)
+    n, d = 20_003, 37
+    budget = _budget(n, d, prec, 4, 4) if streamed else None
+    for i, k in ((0, 0), (n - 1, d - 1), (15_000, 11)):
+        V = rng.standard_normal((n, d)).astype(np.float32)
+        V[i, k] = bad
+        with pytest.raises(pb.InvalidDataError):
+            pb.build_ground_set(V, precision=prec, device_budget=budget)
+    # finite data passes, and float64 input overflowing binary32 keeps the
+    # reference semantics (validated on the host, stored as inf, accepted)
+    V = rng.standard_normal((n, d)).astype(np.float32)
+    g = pb.build_ground_set(V, precision=prec, device_budget=budget)
+    assert np.isfinite(g.aux_loss)
+    if prec is P32:
+        W = V.astype(np.float64)
+        W[5, 3] = 1e39
+        g = pb.build_ground_set(W, precision=prec)
+        assert np.isinf(g.matrix[5, 3]) and np.isinf(g.aux_loss)

@@ -91,7 +91,7 @@ def test_bad_args_fail_without_gpu(native_lib):
 
     with pytest.raises(DimensionMismatchError):
         native_lib.ground_prepare(N.F32, None, 0, 3, None, None, 256, None,
-                                  None, None, None, None)
+                                  None, None, None, 0, None)
     with pytest.raises(DimensionMismatchError):
         native_lib.greedy_gains_simt(N.F32, None, 256, None, 10, None, 256,
                                      None, None, 10, 3, 100, None, 1, None)
