@@ -50,7 +50,7 @@ extern "C" {
 #define EXEM_ERR_UNSUPPORTED 5 /* ExemError: no sm_100a device / bad dtype   */
 
 const char *exem_last_error(void);
-int exem_abi_version(void);
+int exem_abi_version(void); /* 2: check_finite in K1, interleaved K4-TC set tiles */
 
 /* Device query: SM count, compute capability, opt-in shared memory. */
 int exem_device_info(int device, int *sm_count, int *cc_major, int *cc_minor,

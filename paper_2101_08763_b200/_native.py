@@ -151,6 +151,12 @@ def raise_status(rc: int, msg: str):
     raise ExemError(f"native error {rc}: {msg}")
 
 
+# Bumped whenever an entry point's signature or contract changes
+# (2: exem_ground_prepare[_rows] gained check_finite; K4-TC set tiles are
+# column-interleaved).
+ABI_VERSION = 2
+
+
 def load_library(path: Path | str | None = None) -> _Lib:
     """Load (once) and bind ``libexem_b200.so``; raise if it is missing."""
     global _lib
@@ -165,6 +171,11 @@ def load_library(path: Path | str | None = None) -> _Lib:
                 "fallback)"
             )
         lib = _Lib(ctypes.CDLL(str(p)))
+        got = int(lib.abi_version())
+        if got != ABI_VERSION:
+            raise ExemError(
+                f"native library {p} has ABI {got}, this package needs "
+                f"{ABI_VERSION}: rebuild it (python -m paper_2101_08763_b200.build)")
         if path is None:
             _lib = lib
         return lib

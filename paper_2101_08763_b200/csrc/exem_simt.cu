@@ -888,7 +888,7 @@ using namespace exem;
 extern "C" {
 
 const char *exem_last_error(void) { return g_err; }
-int exem_abi_version(void) { return 1; }
+int exem_abi_version(void) { return 2; }
 int64_t exem_launch_count(void) {
   return (int64_t)__atomic_load_n(&g_launches, __ATOMIC_RELAXED);
 }
