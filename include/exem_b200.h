@@ -313,6 +313,12 @@ int exem_pack_elements(int dtype, const void *rows, const int64_t *offsets,
                        const int32_t *card, int64_t l, int64_t l_pad,
                        int64_t k_max, int64_t d, void *packed, void *stream);
 
+/* The packed batch as PackedBatch.values holds it (storage dtype,
+ * [d][k_max][l], pkg/src/exembatch/core.py:331-346) widened to the compute
+ * type and zero padded to [d_pad][k_max][l_pad] on the device. */
+int exem_widen_packed(int dtype, const void *src, int64_t l, int64_t l_pad,
+                      int64_t k_max, int64_t d, void *packed, void *stream);
+
 /* pnorms[e][j] = ||S_j[e]||^2 of a packed [d_pad][k_max][l_pad] batch
  * (the element norms e2 of objective.py:84, computed once per batch). */
 int exem_packed_norms(int dtype, const void *packed, int64_t d, int64_t k_max,

@@ -105,6 +105,8 @@ _SIGNATURES = {
     "exem_ground_prepare_rows": (c_int, [c_int, _P, c_int64, c_int64, _P, _P,
                                          c_int64, _P, _P, _P, _P, c_int, _P]),
     "exem_h2d_bytes": (c_int, [_P, _P, c_int64, _P]),
+    "exem_widen_packed": (c_int, [c_int, _P, c_int64, c_int64, c_int64,
+                                  c_int64, _P, _P]),
     "exem_launch_count": (c_int64, []),
 }
 

@@ -880,6 +880,27 @@ __global__ void pack_elements_kernel(
   }
 }
 
+// A packed round-robin batch as the host holds it -- storage dtype,
+// [d][k_max][l] (PackedBatch.values, core.py:331-346) -- widened to the
+// compute type and zero padded to [d_pad][k_max][l_pad] on the device, so the
+// host uploads the raw packed bytes instead of converting them.
+template <int DT>
+__global__ void widen_packed_kernel(const typename Traits<DT>::S *__restrict__ src,
+                                    int64_t l, int64_t l_pad, int k_max, int d,
+                                    int d_pad,
+                                    typename Traits<DT>::C *__restrict__ dst) {
+  using C = typename Traits<DT>::C;
+  const int64_t j = (int64_t)blockIdx.x * 128 + threadIdx.x;
+  const int e = blockIdx.y;
+  if (j >= l_pad) return;
+  for (int k = blockIdx.z; k < d_pad; k += gridDim.z) {
+    const C v = (k < d && j < l)
+                    ? to_c(src[((int64_t)k * k_max + e) * l + j])
+                    : C(0);
+    dst[((int64_t)k * k_max + e) * l_pad + j] = v;
+  }
+}
+
 }  // namespace exem
 
 using namespace exem;
@@ -1233,6 +1254,24 @@ int exem_pack_elements(int dtype, const void *rows, const int64_t *offsets,
         (const S *)rows, offsets, card, l, l_pad, (int)k_max, (int)d, d_pad,
         (C *)packed);
     EXEM_LAUNCH_CHECK("pack_elements_kernel");
+  });
+  return EXEM_OK;
+}
+
+int exem_widen_packed(int dtype, const void *src, int64_t l, int64_t l_pad,
+                      int64_t k_max, int64_t d, void *packed, void *stream) {
+  if (l < 1 || k_max < 1 || d < 1 || l_pad < l || k_max > 65535)
+    return fail(EXEM_ERR_ARG, "widen_packed: bad shape");
+  const int d_pad = (int)exem_pad_dims(d);
+  const int zs = d_pad < 64 ? d_pad : 64;
+  dim3 grid((unsigned)ceil_div(l_pad, 128), (unsigned)k_max, (unsigned)zs);
+  cudaStream_t st = (cudaStream_t)stream;
+  EXEM_DISPATCH(dtype, DT, {
+    using S = typename Traits<DT>::S;
+    using C = typename Traits<DT>::C;
+    widen_packed_kernel<DT><<<grid, 128, 0, st>>>(
+        (const S *)src, l, l_pad, (int)k_max, (int)d, d_pad, (C *)packed);
+    EXEM_LAUNCH_CHECK("widen_packed_kernel");
   });
   return EXEM_OK;
 }

@@ -69,11 +69,16 @@ def compute_torch_dtype(precision):
 
 
 def to_device_bytes(arr: np.ndarray, dev):
-    """Upload a numpy array's raw bytes (any dtype, incl. bf16) to ``dev``."""
+    """Upload a numpy array's raw bytes (any dtype, incl. bf16) to ``dev``:
+    one DMA straight from the array (read-only / frozen arrays included, no
+    staging copy), ordered on ``dev``'s current stream."""
     t = torch()
-    raw = np.ascontiguousarray(arr).reshape(-1).view(np.uint8)
-    host = t.from_numpy(raw.copy() if not raw.flags.writeable else raw)
-    return host.to(dev, non_blocking=False)
+    raw = np.ascontiguousarray(arr)
+    with t.cuda.device(dev):
+        out = t.empty(max(raw.nbytes, 1), dtype=t.uint8, device=dev)
+        N.lib().h2d_bytes(N.ptr(out), N.c_void_p(raw.ctypes.data),
+                          raw.nbytes, N.stream_handle(dev))
+    return out[: raw.nbytes]
 
 
 def padded_rows(rows: np.ndarray, d_pad: int, precision, dev):

@@ -174,12 +174,14 @@ class DeviceBatch:
             lib.pack_elements(precision.tag, N.ptr(rows_d), N.ptr(offs_d),
                               N.ptr(card_d), l, self.l_pad, k_max, d,
                               N.ptr(self.packed), stream)
-        else:
-            host = np.zeros((d_pad, k_max, self.l_pad),
-                            dtype=precision.compute_dtype)
-            host[:d, :, :l] = np.asarray(values, dtype=precision.dtype).reshape(
-                d, k_max, l).astype(precision.compute_dtype)
-            self.packed = t.from_numpy(host).to(dev)
+        else:  # raw packed bytes up, widened + padded on the device
+            raw = np.ascontiguousarray(
+                np.asarray(values, dtype=precision.dtype).reshape(d, k_max, l))
+            raw_d = to_device_bytes(raw, dev)
+            self.packed = t.empty((d_pad, k_max, self.l_pad), dtype=cdt,
+                                  device=dev)
+            lib.widen_packed(precision.tag, N.ptr(raw_d), l, self.l_pad, k_max,
+                             d, N.ptr(self.packed), stream)
         self.pnorms = t.empty((k_max, self.l_pad), dtype=t.float64, device=dev)
         lib.packed_norms(precision.tag, N.ptr(self.packed), d, k_max,
                          self.l_pad, N.ptr(self.pnorms), stream)
