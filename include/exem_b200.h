@@ -328,6 +328,20 @@ int exem_packed_norms(int dtype, const void *packed, int64_t d, int64_t k_max,
 int exem_row_norms(int dtype, const void *x, int64_t rows, int64_t d,
                    int64_t d_pad, double *out, void *stream);
 
+/* SieveStreaming over a BLOCK of nb arriving elements (sieve.py):
+ * exem_sieve_block_dist writes dist[b][i] = d(v_i, elems[b]) with K2's
+ * arithmetic (identical to exem_set_min, k = 1); exem_sieve_block_gains then
+ * computes gains[s][b] = sum_i max(0, M[s][i] - dist[b][i]) for every sieve
+ * row s < rows (fp64, fixed order), scratch = exem_sieve_block_scratch. */
+int exem_sieve_block_dist(int dtype, const void *vt, int64_t ld, int64_t n,
+                          int64_t d, const double *norms, const void *elems,
+                          const double *enorms, int64_t nb, void *dist,
+                          int64_t ldd, double *scratch, void *stream);
+int64_t exem_sieve_block_scratch(int64_t n, int64_t rows, int64_t nb);
+int exem_sieve_block_gains(int dtype, const void *M, int64_t ldm, int64_t rows,
+                           const void *D, int64_t ldd, int64_t nb, int64_t n,
+                           double *gains, double *scratch, void *stream);
+
 /*
  * Sieve streaming (north star: "the Greedy and streaming optimizers"; the
  * reference ships none, SPEC.md:9,402 -- see sieve.py).  Each sieve s keeps

@@ -107,6 +107,12 @@ _SIGNATURES = {
     "exem_h2d_bytes": (c_int, [_P, _P, c_int64, _P]),
     "exem_widen_packed": (c_int, [c_int, _P, c_int64, c_int64, c_int64,
                                   c_int64, _P, _P]),
+    "exem_sieve_block_dist": (c_int, [c_int, _P, c_int64, c_int64, c_int64,
+                                      _P, _P, _P, c_int64, _P, c_int64, _P,
+                                      _P]),
+    "exem_sieve_block_scratch": (c_int64, [c_int64, c_int64, c_int64]),
+    "exem_sieve_block_gains": (c_int, [c_int, _P, c_int64, c_int64, _P,
+                                       c_int64, c_int64, c_int64, _P, _P, _P]),
     "exem_launch_count": (c_int64, []),
 }
 

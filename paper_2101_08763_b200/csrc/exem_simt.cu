@@ -198,7 +198,9 @@ __global__ void __launch_bounds__(kRedThreads)
                    const double *__restrict__ enorms, int k, int include_aux,
                    typename Traits<DT>::C *__restrict__ t_out,
                    int64_t *__restrict__ label_out,
-                   double *__restrict__ partials) {
+                   double *__restrict__ partials,
+                   typename Traits<DT>::C *__restrict__ dist_out = nullptr,
+                   int64_t ldd = 0) {
   using C = typename Traits<DT>::C;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C *se = reinterpret_cast<C *>(smem_raw);  // [kSetChunk][d_pad]
@@ -256,6 +258,7 @@ __global__ void __launch_bounds__(kRedThreads)
           C dist = Traits<DT>::kDirect
                        ? acc[e]
                        : gemm_form<C>(acc[e], ai, (C)enorms[e0 + e]);
+          if (dist_out) dist_out[(int64_t)(e0 + e) * ldd + i] = dist;
           if (dist < best) {  // strict: lowest element index wins ties
             best = dist;
             lab = e0 + e;
@@ -901,6 +904,69 @@ __global__ void widen_packed_kernel(const typename Traits<DT>::S *__restrict__ s
   }
 }
 
+// SieveStreaming over a block of arriving elements: for every sieve row s
+// (rows of M, row 0 = aux) and block element b,
+//   partial[cta][s][b] = sum_{i in the CTA's points} max(0, M[s][i] - D[b][i])
+// 256 threads as 16 x 16, each a 4 (rows) x 4 (elements) register tile of
+// fp64 sums; M and D are staged 32 points at a time (coalesced).  A 64 x 64
+// (rows x elements) tile per grid.y / grid.z index.
+constexpr int kSbTile = 64, kSbPts = 32;
+
+template <typename C>
+__global__ void __launch_bounds__(256)
+    sieve_block_gains_kernel(const C *__restrict__ M, int64_t ldm, int rows,
+                             const C *__restrict__ D, int64_t ldd, int nb,
+                             int64_t n, int64_t pts_per_cta,
+                             double *__restrict__ partial) {
+  __shared__ C Ms[kSbTile][kSbPts + 1];
+  __shared__ C Ds[kSbTile][kSbPts + 1];
+  const int ts = threadIdx.x >> 4, tb = threadIdx.x & 15;
+  const int r0 = blockIdx.y * kSbTile, b0 = blockIdx.z * kSbTile;
+  const int64_t p0 = (int64_t)blockIdx.x * pts_per_cta;
+  const int64_t p1 = min(n, p0 + pts_per_cta);
+  double acc[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+  for (int64_t q = p0; q < p1; q += kSbPts) {
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < kSbTile * kSbPts; idx += 256) {
+      const int r = idx / kSbPts, c = idx % kSbPts;
+      const int64_t i = q + c;
+      // padding points contribute max(0, 0 - 0) = 0
+      Ms[r][c] = (r0 + r < rows && i < p1) ? M[(int64_t)(r0 + r) * ldm + i] : C(0);
+      Ds[r][c] = (b0 + r < nb && i < p1) ? D[(int64_t)(b0 + r) * ldd + i] : C(0);
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int c = 0; c < kSbPts; ++c) {
+      C m[4], dd[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) m[u] = Ms[ts * 4 + u][c];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) dd[v] = Ds[tb * 4 + v][c];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+          acc[u][v] += (double)tmax(m[u] - dd[v], C(0));
+    }
+  }
+  // partial[cta][r][b] over the full (rows x nb) output
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int r = r0 + ts * 4 + u;
+    if (r >= rows) continue;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int b = b0 + tb * 4 + v;
+      if (b < nb)
+        partial[((int64_t)blockIdx.x * rows + r) * nb + b] = acc[u][v];
+    }
+  }
+}
+
 }  // namespace exem
 
 using namespace exem;
@@ -1274,6 +1340,64 @@ int exem_widen_packed(int dtype, const void *src, int64_t l, int64_t l_pad,
     EXEM_LAUNCH_CHECK("widen_packed_kernel");
   });
   return EXEM_OK;
+}
+
+int exem_sieve_block_dist(int dtype, const void *vt, int64_t ld, int64_t n,
+                          int64_t d, const double *norms, const void *elems,
+                          const double *enorms, int64_t nb, void *dist,
+                          int64_t ldd, double *scratch, void *stream) {
+  if (n < 1 || d < 1 || nb < 1 || ldd < n)
+    return fail(EXEM_ERR_ARG, "sieve_block_dist: bad shape");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int d_pad = (int)exem_pad_dims(d);
+  const int64_t blocks = ceil_div(n, kRedThreads);
+  EXEM_DISPATCH(dtype, DT, {
+    using C = typename Traits<DT>::C;
+    size_t smem = (size_t)kSetChunk * d_pad * sizeof(C);
+    if (smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(
+          set_min_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+          (int)smem);
+      if (e != cudaSuccess)
+        return fail(EXEM_ERR_CUDA, "set_min smem: %s", cudaGetErrorString(e));
+    }
+    // K2's distance arithmetic (bit-identical to exem_set_min with k = 1),
+    // every element's distance row written out
+    set_min_kernel<DT><<<(unsigned)blocks, kRedThreads, smem, st>>>(
+        (const C *)vt, ld, n, (int)d, norms, nullptr, (const C *)elems, d_pad,
+        enorms, (int)nb, 0, nullptr, nullptr, scratch, (C *)dist, ldd);
+    EXEM_LAUNCH_CHECK("set_min_kernel(dist)");
+  });
+  return EXEM_OK;
+}
+
+int64_t exem_sieve_block_scratch(int64_t n, int64_t rows, int64_t nb) {
+  const int64_t ctas = n < 32 * 296 ? ceil_div(n, 32) : 296;
+  return ctas * rows * nb;
+}
+
+int exem_sieve_block_gains(int dtype, const void *M, int64_t ldm, int64_t rows,
+                           const void *D, int64_t ldd, int64_t nb, int64_t n,
+                           double *gains, double *scratch, void *stream) {
+  if (n < 1 || rows < 1 || nb < 1 || ldm < n || ldd < n)
+    return fail(EXEM_ERR_ARG, "sieve_block_gains: bad shape");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t ctas = n < 32 * 296 ? ceil_div(n, 32) : 296;
+  const int64_t per = round_up(ceil_div(n, ctas), kSbPts);
+  const int64_t used = ceil_div(n, per);
+  dim3 grid((unsigned)used, (unsigned)ceil_div(rows, kSbTile),
+            (unsigned)ceil_div(nb, kSbTile));
+  if (dtype == EXEM_F64)
+    sieve_block_gains_kernel<double><<<grid, 256, 0, st>>>(
+        (const double *)M, ldm, (int)rows, (const double *)D, ldd, (int)nb, n,
+        per, scratch);
+  else
+    sieve_block_gains_kernel<float><<<grid, 256, 0, st>>>(
+        (const float *)M, ldm, (int)rows, (const float *)D, ldd, (int)nb, n,
+        per, scratch);
+  EXEM_LAUNCH_CHECK("sieve_block_gains_kernel");
+  // fixed-order sum over the CTAs' point chunks
+  return exem_reduce_partials(scratch, used, rows * nb, 1.0, gains, stream);
 }
 
 int exem_sieve_gains(int dtype, const void *M, int64_t ldm, int64_t sieves,

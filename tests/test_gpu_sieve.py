@@ -52,3 +52,22 @@ def test_sieve_argument_errors():
     with pytest.raises(ValueError):
         pb.sieve_streaming_maximize(g, 2, eps=0.0)
     assert pb.sieve_streaming_maximize(g, 0).exemplar_indices == ()
+
+
+@pytest.mark.parametrize("prec", [Precision.binary64, Precision.binary32])
+def test_sieve_block_size_invariant(prec):
+    """Block processing (one distance pass + one scoring launch per block,
+    rescoring only a sieve that just grew) makes the element-at-a-time
+    decisions: same picks and values for every block size, including a
+    stream order that revisits nothing and ends mid-block."""
+    rng = np.random.default_rng(4)
+    V = rng.standard_normal((2500, 12))
+    g = pb.build_ground_set(V, precision=prec)
+    order = rng.permutation(2500)[:2333]
+    ref = pb.sieve_streaming_maximize(g, 7, eps=0.15, order=order, block=1)
+    for block in (5, 64, 300):
+        res = pb.sieve_streaming_maximize(g, 7, eps=0.15, order=order,
+                                          block=block)
+        assert res.exemplar_indices == ref.exemplar_indices, block
+        assert res.values == ref.values
+        assert res.evaluations == ref.evaluations
