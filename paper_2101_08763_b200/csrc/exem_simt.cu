@@ -90,11 +90,32 @@ __global__ void __launch_bounds__(kRedThreads)
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   double nrm = 0.0, dst = 0.0;
   if (i < ld) {
-    for (int k = 0; k < d_pad; ++k) {
+    // HBM-bound: kLoadAheadK1 independent coalesced loads in flight per
+    // thread, then the stores and the (same-order) fp64 accumulations
+    constexpr int kLoadAheadK1 = 8;
+    const bool live = i < n;
+    int k = 0;
+    for (; k + kLoadAheadK1 <= d; k += kLoadAheadK1) {
+      C xs[kLoadAheadK1];
+#pragma unroll
+      for (int u = 0; u < kLoadAheadK1; ++u)
+        xs[u] = live ? to_c(src[(int64_t)(k + u) * n + i]) : C(0);
+#pragma unroll
+      for (int u = 0; u < kLoadAheadK1; ++u) {
+        vt[(int64_t)(k + u) * ld + i] = xs[u];
+        if (live) {
+          double xd = (double)xs[u];
+          nrm += xd * xd;
+          double df = xd - (double)to_c(e0[k + u]);
+          dst += df * df;
+        }
+      }
+    }
+    for (; k < d_pad; ++k) {
       C x = C(0);
-      if (k < d && i < n) x = to_c(src[(int64_t)k * n + i]);
+      if (k < d && live) x = to_c(src[(int64_t)k * n + i]);
       vt[(int64_t)k * ld + i] = x;
-      if (k < d && i < n) {
+      if (k < d && live) {
         double xd = (double)x;
         nrm += xd * xd;
         double df = xd - (double)to_c(e0[k]);
@@ -143,11 +164,21 @@ __global__ void __launch_bounds__(kRedThreads)
   double nrm = 0.0, dst = 0.0;
   for (int k0 = 0; k0 < d_pad; k0 += 32) {
     __syncthreads();
-    for (int idx = threadIdx.x; idx < kRedThreads * 32; idx += kRedThreads) {
+    // 32 loads per thread, all issued before any shared-memory store
+    // (memory-level parallelism; each warp reads one row segment per load)
+    C xs[32];
+#pragma unroll
+    for (int u = 0; u < 32; ++u) {
+      const int idx = threadIdx.x + u * kRedThreads;
       const int pp = idx >> 5, kk = idx & 31;
       const int64_t ip = i0 + pp;
       const int k = k0 + kk;
-      tile[pp][kk] = (k < d && ip < n) ? to_c(src[ip * d + k]) : C(0);
+      xs[u] = (k < d && ip < n) ? to_c(src[ip * d + k]) : C(0);
+    }
+#pragma unroll
+    for (int u = 0; u < 32; ++u) {
+      const int idx = threadIdx.x + u * kRedThreads;
+      tile[idx >> 5][idx & 31] = xs[u];
     }
     __syncthreads();
     if (i < ld) {
