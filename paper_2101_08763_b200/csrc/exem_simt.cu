@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(kRedThreads)
 constexpr int kSetChunk = 8;
 constexpr int kLoadAhead = 8;  // independent V loads in flight per thread
 
-template <int DT>
+template <int DT, int CH>
 __global__ void __launch_bounds__(kRedThreads)
     set_min_kernel(const typename Traits<DT>::C *__restrict__ vt, int64_t ld,
                    int64_t n, int d, const double *__restrict__ norms,
@@ -234,22 +234,22 @@ __global__ void __launch_bounds__(kRedThreads)
                    int64_t ldd = 0) {
   using C = typename Traits<DT>::C;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  C *se = reinterpret_cast<C *>(smem_raw);  // [kSetChunk][d_pad]
+  C *se = reinterpret_cast<C *>(smem_raw);  // [CH][d_pad]
   __shared__ double sh[32];
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool live = i < n;
   const C ai = live ? (C)norms[i] : C(0);
   C best = tinf<C>();
   int64_t lab = 0;
-  for (int e0 = 0; e0 < k; e0 += kSetChunk) {
-    const int ec = min(kSetChunk, k - e0);
+  for (int e0 = 0; e0 < k; e0 += CH) {
+    const int ec = min(CH, k - e0);
     __syncthreads();
     for (int idx = threadIdx.x; idx < ec * d_pad; idx += blockDim.x)
       se[idx] = elems[(int64_t)e0 * d_pad + idx];
     __syncthreads();
-    C acc[kSetChunk];
+    C acc[CH];
 #pragma unroll
-    for (int e = 0; e < kSetChunk; ++e) acc[e] = C(0);
+    for (int e = 0; e < CH; ++e) acc[e] = C(0);
     if (live) {
       // HBM-bound: issue kLoadAhead independent coalesced loads per thread
       // before using them (memory-level parallelism), then the FMAs
@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(kRedThreads)
 #pragma unroll
         for (int u = 0; u < kLoadAhead; ++u)
 #pragma unroll
-          for (int e = 0; e < kSetChunk; ++e) {
+          for (int e = 0; e < CH; ++e) {
             if (Traits<DT>::kDirect) {
               const C df = xs[u] - se[e * d_pad + kk + u];
               acc[e] = fma(df, df, acc[e]);
@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(kRedThreads)
       for (; kk < d; ++kk) {
         const C x = vt[(int64_t)kk * ld + i];
 #pragma unroll
-        for (int e = 0; e < kSetChunk; ++e) {
+        for (int e = 0; e < CH; ++e) {
           if (Traits<DT>::kDirect) {
             const C df = x - se[e * d_pad + kk];
             acc[e] = fma(df, df, acc[e]);
@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(kRedThreads)
         }
       }
 #pragma unroll
-      for (int e = 0; e < kSetChunk; ++e) {
+      for (int e = 0; e < CH; ++e) {
         if (e < ec) {
           C dist = Traits<DT>::kDirect
                        ? acc[e]
@@ -306,6 +306,50 @@ __global__ void __launch_bounds__(kRedThreads)
   }
   double r = block_sum<kRedThreads>(live ? (double)t : 0.0, sh);
   if (threadIdx.x == 0) partials[blockIdx.x] = r;
+}
+
+// Element chunk CH = the smallest of 1, 2, 4, 8 covering k (k < 8 computes
+// no dead dot products); the per-element accumulation order is the same for
+// every CH, so the distances are identical.
+template <int DT, int CH>
+static cudaError_t launch_set_min_ch(
+    int64_t blocks, cudaStream_t st, const typename Traits<DT>::C *vt,
+    int64_t ld, int64_t n, int d, const double *norms,
+    const typename Traits<DT>::C *aux, const typename Traits<DT>::C *elems,
+    int d_pad, const double *enorms, int k, int include_aux,
+    typename Traits<DT>::C *t_out, int64_t *label_out, double *partials,
+    typename Traits<DT>::C *dist_out, int64_t ldd) {
+  using C = typename Traits<DT>::C;
+  const size_t smem = (size_t)CH * d_pad * sizeof(C);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(
+        set_min_kernel<DT, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  set_min_kernel<DT, CH><<<(unsigned)blocks, kRedThreads, smem, st>>>(
+      vt, ld, n, d, norms, aux, elems, d_pad, enorms, k, include_aux, t_out,
+      label_out, partials, dist_out, ldd);
+  return cudaGetLastError();
+}
+
+template <int DT>
+static cudaError_t launch_set_min(
+    int64_t blocks, cudaStream_t st, const typename Traits<DT>::C *vt,
+    int64_t ld, int64_t n, int d, const double *norms,
+    const typename Traits<DT>::C *aux, const typename Traits<DT>::C *elems,
+    int d_pad, const double *enorms, int k, int include_aux,
+    typename Traits<DT>::C *t_out, int64_t *label_out, double *partials,
+    typename Traits<DT>::C *dist_out = nullptr, int64_t ldd = 0) {
+#define EXEM_SM(CHN)                                                        \
+  return launch_set_min_ch<DT, CHN>(blocks, st, vt, ld, n, d, norms, aux,   \
+                                    elems, d_pad, enorms, k, include_aux,   \
+                                    t_out, label_out, partials, dist_out, ldd)
+  if (k >= 8) EXEM_SM(8);
+  if (k >= 4) EXEM_SM(4);
+  if (k >= 2) EXEM_SM(2);
+  EXEM_SM(1);
+#undef EXEM_SM
 }
 
 // ============================================================ greedy m init
@@ -1129,18 +1173,13 @@ int exem_set_min(int dtype, const void *vt, int64_t ld, int64_t n, int64_t d,
   const int64_t blocks = ceil_div(n, kRedThreads);
   EXEM_DISPATCH(dtype, DT, {
     using C = typename Traits<DT>::C;
-    size_t smem = (size_t)kSetChunk * d_pad * sizeof(C);
-    if (smem > 48 * 1024) {
-      cudaError_t e = cudaFuncSetAttribute(
-          set_min_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-          (int)smem);
-      if (e != cudaSuccess)
-        return fail(EXEM_ERR_CUDA, "set_min smem: %s", cudaGetErrorString(e));
-    }
-    set_min_kernel<DT><<<(unsigned)blocks, kRedThreads, smem, st>>>(
-        (const C *)vt, ld, n, (int)d, norms, (const C *)aux, (const C *)elems,
-        d_pad, enorms, (int)k, include_aux, (C *)t_out, label_out, scratch);
-    EXEM_LAUNCH_CHECK("set_min_kernel");
+    cudaError_t e = launch_set_min<DT>(
+        blocks, st, (const C *)vt, ld, n, (int)d, norms, (const C *)aux,
+        (const C *)elems, d_pad, enorms, (int)k, include_aux, (C *)t_out,
+        label_out, scratch);
+    if (e != cudaSuccess)
+      return fail(EXEM_ERR_CUDA, "set_min_kernel: %s", cudaGetErrorString(e));
+    count_launch();
   });
   if (sum_out) return reduce_fixed(scratch, blocks, sum_out, 0, st);
   return EXEM_OK;
@@ -1384,20 +1423,16 @@ int exem_sieve_block_dist(int dtype, const void *vt, int64_t ld, int64_t n,
   const int64_t blocks = ceil_div(n, kRedThreads);
   EXEM_DISPATCH(dtype, DT, {
     using C = typename Traits<DT>::C;
-    size_t smem = (size_t)kSetChunk * d_pad * sizeof(C);
-    if (smem > 48 * 1024) {
-      cudaError_t e = cudaFuncSetAttribute(
-          set_min_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-          (int)smem);
-      if (e != cudaSuccess)
-        return fail(EXEM_ERR_CUDA, "set_min smem: %s", cudaGetErrorString(e));
-    }
-    // K2's distance arithmetic (bit-identical to exem_set_min with k = 1),
+    // K2's distance arithmetic (identical to exem_set_min with k = 1),
     // every element's distance row written out
-    set_min_kernel<DT><<<(unsigned)blocks, kRedThreads, smem, st>>>(
-        (const C *)vt, ld, n, (int)d, norms, nullptr, (const C *)elems, d_pad,
-        enorms, (int)nb, 0, nullptr, nullptr, scratch, (C *)dist, ldd);
-    EXEM_LAUNCH_CHECK("set_min_kernel(dist)");
+    cudaError_t e = launch_set_min<DT>(
+        blocks, st, (const C *)vt, ld, n, (int)d, norms, nullptr,
+        (const C *)elems, d_pad, enorms, (int)nb, 0, nullptr, nullptr, scratch,
+        (C *)dist, ldd);
+    if (e != cudaSuccess)
+      return fail(EXEM_ERR_CUDA, "set_min_kernel(dist): %s",
+                  cudaGetErrorString(e));
+    count_launch();
   });
   return EXEM_OK;
 }
