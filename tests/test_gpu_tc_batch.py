@@ -53,9 +53,9 @@ def _check(g, sets, vals, nref=None):
 
 @pytest.mark.parametrize("prec", [BF16, P16])
 @pytest.mark.parametrize("n,d,l,kmin,kmax", [
-    (3000, 100, 150, 1, 50),      # ragged, 4 sets/tile of 56 columns
-    (1000, 2, 70, 1, 1),          # k_max = 1: 16 sets of 8 columns per tile
-    (2500, 16, 45, 8, 8),         # exact multiple-of-8 sets
+    (3000, 100, 150, 1, 50),      # ragged, 5 interleaved sets in N = 256
+    (1000, 2, 70, 1, 1),          # k_max = 1: 16 sets in N = 16
+    (2500, 16, 45, 8, 8),         # 16 sets of 8 in N = 128
     (1300, 256, 20, 1, 256),      # one set per tile, per-chunk point stages
     (777, 700, 9, 3, 40),         # streamed set tile (d > stationary budget)
     (20_000, 37, 33, 1, 12),      # several splits, n % 128 != 0
