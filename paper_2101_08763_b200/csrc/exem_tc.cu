@@ -172,10 +172,9 @@ __device__ __forceinline__ void mma_item_waits(
         fence_after();
       }
       constexpr uint32_t kA = 128 * 128 >> 4, kB = 256 * 128 >> 4;
-      if (!(p.dbg & 2))  // timing experiment: no MMA
-        umma_f16(d, a_desc0 + (uint64_t)((ks >> 2) * kA + (ks & 3) * 2),
-                 b0 + (uint64_t)((ks >> 2) * kB + (ks & 3) * 2), p.idesc,
-                 ks > 0 ? 1u : 0u);
+      umma_f16(d, a_desc0 + (uint64_t)((ks >> 2) * kA + (ks & 3) * 2),
+               b0 + (uint64_t)((ks >> 2) * kB + (ks & 3) * 2), p.idesc,
+               ks > 0 ? 1u : 0u);
     }
     if constexpr (CS > 1)  // every cluster CTA's B stage (multicast)
       umma_commit_mc(&empty[s.stage], (uint16_t)((1u << CS) - 1));
@@ -376,7 +375,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const int64_t p0 = sp * p.split_pts;
         const int64_t p1 = min(p.n, p0 + p.split_pts);
-        if (p.tile_stage && p.ksteps <= 8 && (p.dbg & ~39) == 0) {
+        if (p.tile_stage && p.ksteps <= 8 && (p.dbg & ~5) == 0) {
           // software-pipelined handshake (see mma_item_waits)
           const int ntiles = (int)((p1 - p0 + BN - 1) / BN);
           MmaState ms{stage, ph, tph, buf, tile_no};
@@ -400,7 +399,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tile_no = ms.tile_no;
         }
         for (int64_t pt = p0;
-             pt < p1 && !(p.tile_stage && p.ksteps <= 8 && (p.dbg & ~39) == 0);
+             pt < p1 && !(p.tile_stage && p.ksteps <= 8 && (p.dbg & ~5) == 0);
              pt += BN) {
           TR(0, tile_no);
           mbar_wait(&tempty[buf], ((tph >> buf) & 1u) ^ 1u);
@@ -506,14 +505,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         fence_after();
         const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) +
                                (uint32_t)(buf * BN + half * 128);
-        if (p.dbg & 32) {  // timing experiment: no TMEM drain at all
-          fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[buf]);
-          buf ^= 1u;
-          ++tile_no;
-          continue;
-        }
         // Drain this warp's 32x128 slice of the accumulator into registers
         // first and release the TMEM buffer immediately, so the MMA of tile
         // t+2 never waits on this tile's arithmetic.
