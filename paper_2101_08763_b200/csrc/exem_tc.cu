@@ -38,11 +38,19 @@ constexpr int kEpiWarps = 8;
 constexpr int kSmemBudget = 227 * 1024;
 constexpr int kBarBytes = 1024;
 constexpr int kTrace = 256;  // tiles traced on CTA 0 (EXEM_TC_TRACE)
+// CTA-0 timeline (EXEM_TC_TRACE, tools/tc_trace.py): probe builds only
+// (-DEXEM_TC_PROBE_BUILD), like the EXEM_TC_DEBUG masks.
+#ifdef EXEM_TC_PROBE_BUILD
 #define TR(slot, t)                                                        \
   do {                                                                     \
     if (p.trace != nullptr && blockIdx.x == 0 && (t) < kTrace)             \
       p.trace[(slot) * kTrace + (t)] = clock64();                          \
   } while (0)
+#else
+#define TR(slot, t) \
+  do {              \
+  } while (0)
+#endif
 
 // NK back-to-back MMAs over one 64-wide K chunk in a single asm block: the
 // descriptors advance by 32 B (2 in the >>4 address field) per K=16 step.
@@ -216,6 +224,20 @@ __device__ __forceinline__ void relu_acc(const uint32_t (&r)[32], float &se,
 }
 
 
+// Timing-probe switches (EXEM_TC_DEBUG masks, EXEM_TC_WAITS) exist only in
+// a probe build (-DEXEM_TC_PROBE_BUILD via EXEM_NVCC_FLAGS): even untaken,
+// such branches in the issuer / epilogue loops can cost a large share of a
+// step (K3 power wall).
+#ifdef EXEM_TC_PROBE_BUILD
+#define TC_PROBE(p, bit) (((p).dbg & (bit)) != 0)
+#define TC_PROBE_ANY(p, mask) (((p).dbg & (mask)) != 0)
+#define TC_WAIT_SPIN(p) (((p).wait_mode & 8) != 0)
+#else
+#define TC_PROBE(p, bit) false
+#define TC_PROBE_ANY(p, mask) false
+#define TC_WAIT_SPIN(p) false
+#endif
+
 struct Params {
   int64_t l;            // candidates
   int64_t n;            // points of this shard
@@ -324,9 +346,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           // whole-tile stages: one stage = every K chunk of the B tile
           const int per_stage = p.tile_stage ? p.kchunks : 1;
           for (int kc0 = 0; kc0 < p.kchunks; kc0 += per_stage) {
-            if (!(p.dbg & 16)) mbar_wait_sleep(&empty[stage], ph ^ 1);
+            if (!TC_PROBE(p, 16)) mbar_wait_sleep(&empty[stage], ph ^ 1);
             unsigned char *dst = sb + stage * stage_bytes;
-            if (p.dbg & 4) {  // timing experiment: no operand traffic
+            if (TC_PROBE(p, 4)) {  // timing experiment: no operand traffic
               mbar_arrive(&full[stage]);
             } else if (kCS > 1) {
               // this CTA's 1/kCS of the B tile, to every CTA of the cluster
@@ -375,7 +397,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const int64_t p0 = sp * p.split_pts;
         const int64_t p1 = min(p.n, p0 + p.split_pts);
-        if (p.tile_stage && p.ksteps <= 8 && (p.dbg & ~5) == 0) {
+        if (p.tile_stage && p.ksteps <= 8 && !TC_PROBE_ANY(p, ~5)) {
           // software-pipelined handshake (see mma_item_waits)
           const int ntiles = (int)((p1 - p0 + BN - 1) / BN);
           MmaState ms{stage, ph, tph, buf, tile_no};
@@ -399,7 +421,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tile_no = ms.tile_no;
         }
         for (int64_t pt = p0;
-             pt < p1 && !(p.tile_stage && p.ksteps <= 8 && (p.dbg & ~5) == 0);
+             pt < p1 && !(p.tile_stage && p.ksteps <= 8 && !TC_PROBE_ANY(p, ~5));
              pt += BN) {
           TR(0, tile_no);
           mbar_wait(&tempty[buf], ((tph >> buf) & 1u) ^ 1u);
@@ -408,10 +430,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           fence_after();  // TMEM WAR vs the epilogue's tcgen05.ld
           const uint32_t dcol = tmem + buf * (uint32_t)BN;
           if (p.tile_stage) {
-            if (!(p.dbg & 8)) mbar_wait(&full[stage], ph);
+            if (!TC_PROBE(p, 8)) mbar_wait(&full[stage], ph);
             TR(2, tile_no);
-            const uint64_t bd0 = b_desc0 + (uint64_t)(((p.dbg & 128) ? 0 : stage) * stage_step);
-            if (!(p.dbg & 2)) {
+            const uint64_t bd0 = b_desc0 + (uint64_t)((TC_PROBE(p, 128) ? 0 : stage) * stage_step);
+            if (!TC_PROBE(p, 2)) {
               switch (p.ksteps) {  // compile-time K for d <= 122
                 case 1: issue_tile<1>(dcol, a_desc0, bd0, p.idesc); break;
                 case 2: issue_tile<2>(dcol, a_desc0, bd0, p.idesc); break;
@@ -431,7 +453,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                   }
               }
             }
-            if (!(p.dbg & 16)) {
+            if (!TC_PROBE(p, 16)) {
               if constexpr (kCS > 1)
                 umma_commit_mc(&empty[stage], (uint16_t)((1u << kCS) - 1));
               else umma_commit(&empty[stage]);
@@ -450,7 +472,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                   kAStream ? bd + (uint64_t)(B_CHUNK >> 4)
                            : a_desc0 + (uint64_t)(kc * (A_CHUNK >> 4));
               const int nk = ks_left < KCH / 16 ? ks_left : KCH / 16;
-              if (!(p.dbg & 2)) {
+              if (!TC_PROBE(p, 2)) {
 #pragma unroll 1
                 for (int j = 0; j < nk; ++j)
                   umma_f16(dcol, ad + (uint64_t)(2 * j), bd + (uint64_t)(2 * j),
@@ -494,7 +516,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (tr) TR(4, tile_no);
         // one lane polls the barrier; the warp sync orders the others
         if (lane == 0) {
-          if (p.wait_mode & 8)
+          if (TC_WAIT_SPIN(p))
             mbar_wait(&tfull[buf], (tph >> buf) & 1u);
           else
             mbar_wait_sleep(&tfull[buf], (tph >> buf) & 1u);
@@ -518,7 +540,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[buf]);
         if (tr) TR(6, tile_no);
-        if (p.dbg & 1) {  // timing experiment: no epilogue arithmetic
+        if (TC_PROBE(p, 1)) {  // timing experiment: no epilogue arithmetic
           g += (double)__uint_as_float(r0[0] ^ r1[5] ^ r2[9] ^ r3[31]);
           buf ^= 1u;
           ++tile_no;

@@ -67,6 +67,15 @@ constexpr int kTrace = 256;  // tiles traced on CTA 0
   } while (0)
 #endif
 
+// Timing-probe masks (EXEM_TCB_DEBUG: 1 no epilogue, 2 no MMA, 4 no point
+// TMA, 8 no aux load) exist only in a probe build (-DEXEM_TCB_PROBE_BUILD via
+// EXEM_NVCC_FLAGS): K3 showed such branches alone can cost ~20 % of a step.
+#ifdef EXEM_TCB_PROBE_BUILD
+#define TCB_PROBE(p, bit) (((p).dbg & (bit)) != 0)
+#else
+#define TCB_PROBE(p, bit) false
+#endif
+
 struct BParams {
   int64_t n;           // points of this slice
   int64_t l;           // sets
@@ -227,7 +236,7 @@ __device__ __forceinline__ void epilogue_role(const BParams &p, uint32_t tmem,
     for (int64_t pt = p0; pt < p1; pt += BM) {
       const int64_t pi = pt + row;
       const bool valid = pi < p1;
-      const float ax = (valid && !(p.dbg & 8)) ? p.aux[pi] : 0.f;
+      const float ax = (valid && !TCB_PROBE(p, 8)) ? p.aux[pi] : 0.f;
       const float ha = (kPlain && valid) ? (float)p.norms[pi] : 0.f;
       if (lane == 0) {
         mbar_wait_sleep(&tfull[buf], (tph >> buf) & 1u);
@@ -244,7 +253,7 @@ __device__ __forceinline__ void epilogue_role(const BParams &p, uint32_t tmem,
       const uint32_t taddr =
           tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * 256);
       TmemRelease rel{&tempty[buf], lane};
-      if (p.dbg & 1) {  // timing experiment: no TMEM drain / math
+      if (TCB_PROBE(p, 1)) {  // timing experiment: no TMEM drain / math
         rel();
       } else {
 #ifdef EXEM_TCB_TRACE_BUILD
@@ -341,7 +350,7 @@ __device__ __forceinline__ void k4_item_tstage(
         tph ^= 1u << nbuf;
         fence_after();
       }
-      if (!(p.dbg & 2))
+      if (!TCB_PROBE(p, 2))
         umma_f16(d, ad + (uint64_t)((ks >> 2) * (A_CHUNK >> 4) + (ks & 3) * 2),
                  b_base + (uint64_t)((ks >> 2) * b_step + (ks & 3) * 2),
                  p.idesc, ks > 0 ? 1u : 0u);
@@ -370,7 +379,7 @@ __device__ __forceinline__ void k4_item_tstage(
 __device__ __forceinline__ void issue_mma(const BParams &p, uint32_t d,
                                           uint64_t ad, uint64_t bd,
                                           uint32_t b_step, int kc, int j) {
-  if (p.dbg & 2) return;  // timing experiment: no MMA
+  if (TCB_PROBE(p, 2)) return;  // timing experiment: no MMA
   const uint64_t a = ad + (uint64_t)((j >> 2) * (A_CHUNK >> 4) + (j & 3) * 2);
   const uint64_t b = bd + (uint64_t)((j >> 2) * b_step + (j & 3) * 2);
   umma_f16(d, a, b, p.idesc, (kc | j) ? 1u : 0u);
@@ -479,7 +488,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(&empty[stage], ph ^ 1);
             if (kc == 0) TRB(5, ptile);
             unsigned char *dst = sa + stage * stage_bytes;
-            if (p.dbg & 4) {  // timing experiment: no point-operand traffic
+            if (TCB_PROBE(p, 4)) {  // timing experiment: no point-operand traffic
               mbar_arrive(&full[stage]);
             } else {
               mbar_expect_tx(&full[stage],

@@ -1,6 +1,9 @@
 """K4-TC timing experiments: time the batch kernel alone (resident V, CUDA
 events) for a few shapes and EXEM_TCB_DEBUG masks (1: no epilogue math,
-2: no MMA, 4: no point TMA, 8: no aux load).  Run on the GPU box:
+2: no MMA, 4: no point TMA, 8: no aux load; the masks exist only in a probe
+build: EXEM_NVCC_FLAGS=-DEXEM_TCB_PROBE_BUILD python -m
+paper_2101_08763_b200.build, and rebuild normally afterwards).  Run on the
+GPU box:
 
     python tools/k4_probe.py [--n 1000000] [--dims 100,256] [--ks 50]
 """
