@@ -473,10 +473,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                            : a_desc0 + (uint64_t)(kc * (A_CHUNK >> 4));
               const int nk = ks_left < KCH / 16 ? ks_left : KCH / 16;
               if (!TC_PROBE(p, 2)) {
+                // whole chunks from compile-time unrolled code (the single
+                // issuing thread is the critical path; K4-TC measured 1.06-
+                // 1.31x from this), the runtime loop only for a ragged tail
+                if (nk == KCH / 16) {
+#pragma unroll
+                  for (int j = 0; j < KCH / 16; ++j)
+                    umma_f16(dcol, ad + (uint64_t)(2 * j),
+                             bd + (uint64_t)(2 * j), p.idesc,
+                             (kc | j) ? 1u : 0u);
+                } else {
 #pragma unroll 1
-                for (int j = 0; j < nk; ++j)
-                  umma_f16(dcol, ad + (uint64_t)(2 * j), bd + (uint64_t)(2 * j),
-                           p.idesc, (kc | j) ? 1u : 0u);
+                  for (int j = 0; j < nk; ++j)
+                    umma_f16(dcol, ad + (uint64_t)(2 * j),
+                             bd + (uint64_t)(2 * j), p.idesc,
+                             (kc | j) ? 1u : 0u);
+                }
               }
               ks_left -= KCH / 16;
               if constexpr (kCS > 1)

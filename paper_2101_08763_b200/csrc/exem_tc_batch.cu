@@ -587,8 +587,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           const bool trc = kc == 1 || (p.kchunks == 1);
           if (trc) TRB(7, itile);
+          // full events (one or two whole 64-wide chunks) issue from
+          // compile-time unrolled code: the issuing thread is the critical
+          // path (K3's experience), the runtime loop only covers ragged tails
+          if (nk == 8) {
+#pragma unroll
+            for (int j = 0; j < 6; ++j) issue_mma(p, d, ad, bd, b_step, kc, j);
+          } else if (nk == 4) {
+#pragma unroll
+            for (int j = 0; j < 2; ++j) issue_mma(p, d, ad, bd, b_step, kc, j);
+          } else {
 #pragma unroll 1
-          for (int j = 0; j < head; ++j) issue_mma(p, d, ad, bd, b_step, kc, j);
+            for (int j = 0; j < head; ++j) issue_mma(p, d, ad, bd, b_step, kc, j);
+          }
           if (trc) TRB(8, itile);
           if (e + 1 < nev) {
             if (last && !p.late) {
@@ -604,8 +615,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (last) fence_after();
           }
           if (trc) TRB(9, itile);
+          if (nk == 8) {
+#pragma unroll
+            for (int j = 6; j < 8; ++j) issue_mma(p, d, ad, bd, b_step, kc, j);
+          } else if (nk == 4) {
+#pragma unroll
+            for (int j = 2; j < 4; ++j) issue_mma(p, d, ad, bd, b_step, kc, j);
+          } else {
 #pragma unroll 1
-          for (int j = head; j < nk; ++j) issue_mma(p, d, ad, bd, b_step, kc, j);
+            for (int j = head; j < nk; ++j) issue_mma(p, d, ad, bd, b_step, kc, j);
+          }
           if (trc) TRB(10, itile);
           release_stage<MC>(&empty[stage]);
           if (trc) TRB(11, itile);
