@@ -163,6 +163,8 @@ def run_reference(args, rank, world):
     V = synthetic(n, d, args.seed)
     total_sets, total_t = 0, 0.0
     per_step = max(1.0, min(args.cpu_seconds / 4, 4.0))
+    for step in range(args.warmup):  # untimed: worker pool, page-in of V
+        cpu_sample(n, d, args.seed + step, step + 1, 0.25, threads, V)
     for step in range(args.warmup, args.warmup + args.steps):
         set_size = step + 1  # Greedy step t evaluates |S u {c}| = t+1
         rate, cnt, t = cpu_sample(n, d, args.seed + step, set_size, per_step,
