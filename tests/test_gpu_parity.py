@@ -353,3 +353,21 @@ def test_tc_greedy_trajectory(prec):
             assert abs(gains[t][res.exemplar_indices[t]] - top) <= 2e-4 * max(1, top)
             return
     _close(res.values, vals, 2e-4)
+
+
+@pytest.mark.parametrize("prec", [P32, P64, P16, BF16])
+def test_tiled_evaluate_matches_evaluate_batch(prec):
+    """PackedBatch.values uploaded raw and widened/padded on the device
+    (exem_widen_packed) vs the sets interleaved on the device
+    (exem_pack_elements): the same packed layout, so tiled_evaluate and
+    evaluate_batch agree bit for bit (the reference's backend equivalence,
+    tests/test_acceptance.py:46-71)."""
+    rng = np.random.default_rng(13)
+    g = pb.build_ground_set(rng.standard_normal((3000, 29)) *
+                            (0.5 if prec is P16 else 1.0), precision=prec)
+    sets = [g.matrix[rng.choice(3000, int(rng.integers(1, 40)), replace=False)]
+            for _ in range(77)]
+    batch = EvaluationBatch.from_sets(sets)
+    a = pb.evaluate_batch(Evaluator(), g, batch)
+    b = pb.tiled_evaluate(g, pb.pack_batch(batch, g.precision))
+    assert np.array_equal(a, b)
