@@ -487,19 +487,19 @@ constexpr int kBM = 128, kBN = 128, kBK = 8, kThreads = 256;
 
 constexpr int kSimtStages = 3;  // cp.async ring: one barrier per k-chunk
 
-template <typename T>
+template <typename T, int BK = kBK>
 struct SimtSmem {
-  T a[kSimtStages][kBK][kBM];
-  T b[kSimtStages][kBK][kBN];
+  T a[kSimtStages][BK][kBM];
+  T b[kSimtStages][BK][kBN];
 };
 
-template <typename T>
+template <typename T, int BK = kBK>
 __device__ __forceinline__ void load_chunk(T (*dst)[kBM], const T *src,
                                            int64_t ldsrc, int64_t col0,
                                            int k0) {
   constexpr int kVec = 16 / sizeof(T);            // elements per 16B
   constexpr int kPerRow = kBM / kVec;             // 16B packets per row
-  constexpr int kTotal = kBK * kPerRow;           // packets per chunk
+  constexpr int kTotal = BK * kPerRow;            // packets per chunk
 #pragma unroll
   for (int p = threadIdx.x; p < kTotal; p += kThreads) {
     const int row = p / kPerRow, col = (p % kPerRow) * kVec;
@@ -507,11 +507,11 @@ __device__ __forceinline__ void load_chunk(T (*dst)[kBM], const T *src,
   }
 }
 
-template <typename T, bool kDirect>
-__device__ __forceinline__ void mma_chunk(const SimtSmem<T> &sm, int buf,
+template <typename T, bool kDirect, int BK = kBK>
+__device__ __forceinline__ void mma_chunk(const SimtSmem<T, BK> &sm, int buf,
                                           int tx, int ty, T (&acc)[8][8]) {
 #pragma unroll
-  for (int kk = 0; kk < kBK; ++kk) {
+  for (int kk = 0; kk < BK; ++kk) {
     T a[8], b[8];
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
@@ -535,8 +535,8 @@ __device__ __forceinline__ void mma_chunk(const SimtSmem<T> &sm, int buf,
 }
 
 // Full-k mainloop for one (row tile, point tile) pair.
-template <typename T, bool kDirect>
-__device__ __forceinline__ void simt_mainloop(SimtSmem<T> &sm, const T *arow,
+template <typename T, bool kDirect, int BK = kBK>
+__device__ __forceinline__ void simt_mainloop(SimtSmem<T, BK> &sm, const T *arow,
                                               int64_t lda, int64_t a0,
                                               const T *bpts, int64_t ldb,
                                               int64_t b0, int d_pad, int tx,
@@ -545,14 +545,14 @@ __device__ __forceinline__ void simt_mainloop(SimtSmem<T> &sm, const T *arow,
   // group c.  Each iteration waits for its chunk, then ONE barrier both
   // publishes it and proves every thread has finished chunk c-1, whose
   // buffer the load of chunk c+2 then overwrites.
-  const int nk = d_pad / kBK;
+  const int nk = d_pad / BK;
   __syncthreads();  // previous consumers of the ring are done
-  load_chunk<T>(sm.a[0], arow, lda, a0, 0);
-  load_chunk<T>(sm.b[0], bpts, ldb, b0, 0);
+  load_chunk<T, BK>(sm.a[0], arow, lda, a0, 0);
+  load_chunk<T, BK>(sm.b[0], bpts, ldb, b0, 0);
   cp_async_commit();
   if (nk > 1) {
-    load_chunk<T>(sm.a[1], arow, lda, a0, kBK);
-    load_chunk<T>(sm.b[1], bpts, ldb, b0, kBK);
+    load_chunk<T, BK>(sm.a[1], arow, lda, a0, BK);
+    load_chunk<T, BK>(sm.b[1], bpts, ldb, b0, BK);
   }
   cp_async_commit();
   int buf = 0;
@@ -561,11 +561,11 @@ __device__ __forceinline__ void simt_mainloop(SimtSmem<T> &sm, const T *arow,
     __syncthreads();
     if (c + 2 < nk) {
       const int nb = buf == 0 ? 2 : buf - 1;  // (c + 2) % 3
-      load_chunk<T>(sm.a[nb], arow, lda, a0, (c + 2) * kBK);
-      load_chunk<T>(sm.b[nb], bpts, ldb, b0, (c + 2) * kBK);
+      load_chunk<T, BK>(sm.a[nb], arow, lda, a0, (c + 2) * BK);
+      load_chunk<T, BK>(sm.b[nb], bpts, ldb, b0, (c + 2) * BK);
     }
     cp_async_commit();  // (possibly empty: keeps group c+2 = chunk c+2)
-    mma_chunk<T, kDirect>(sm, buf, tx, ty, acc);
+    mma_chunk<T, kDirect, BK>(sm, buf, tx, ty, acc);
     buf = buf == 2 ? 0 : buf + 1;
   }
 }
@@ -578,7 +578,7 @@ __device__ __forceinline__ int tile_off(int t4, int r) {
 //     h_i = (a_i - m_i)/2, b'_c = ||c||^2/2  => 2*that = sum max(0, m_i - d).
 // The per-tile constants live in shared memory to keep the 8x8 register
 // tile spill-free at 2 CTAs/SM.
-template <typename T, int kMinBlocks>
+template <typename T, int kMinBlocks, int BK = kBK>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
     gains_simt_kernel(const T *__restrict__ cvt, int64_t ldc,
                       const double *__restrict__ cnorms, int64_t l,
@@ -587,7 +587,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
                       const T *__restrict__ m, int64_t n, int d_pad,
                       int64_t split_pts, double *__restrict__ partial) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  SimtSmem<T> &sm = *reinterpret_cast<SimtSmem<T> *>(smem_raw);
+  SimtSmem<T, BK> &sm = *reinterpret_cast<SimtSmem<T, BK> *>(smem_raw);
   __shared__ T s_b[kBM];
   __shared__ T s_h[kBN];
   const int tid = threadIdx.x;
@@ -615,7 +615,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 #pragma unroll
       for (int c = 0; c < 8; ++c)
         acc[r][c] = -(s_h[tile_off(tx, c)] + s_b[tile_off(ty, r)]);
-    simt_mainloop<T, false>(sm, cvt, ldc, c0, vt, ld, p0, d_pad, tx, ty, acc);
+    simt_mainloop<T, false, BK>(sm, cvt, ldc, c0, vt, ld, p0, d_pad, tx, ty,
+                                acc);
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
       T s = T(0);
@@ -1246,7 +1247,36 @@ int exem_greedy_gains_simt(int dtype, const void *cvt, int64_t ldc,
   cudaStream_t st = (cudaStream_t)stream;
   const int d_pad = (int)exem_pad_dims(d);
   dim3 grid((unsigned)ceil_div(l, kBM), (unsigned)splits);
-  if (dtype == EXEM_F32) {
+  // fp64: k-chunks of 16 (half the ring barriers per DFMA) when d_pad allows
+  // it without extra padding -- d = 512 / 1024: 436 -> 413 / 866 -> 822 ms;
+  // fp32 measured slower that way (0.75 -> 0.73 of FFMA), kept at 8.
+  // EXEM_SIMT_BK = 8 | 16 overrides (timing experiments).
+  static const int bk_env = getenv("EXEM_SIMT_BK") ? atoi(getenv("EXEM_SIMT_BK")) : 0;
+  const bool bk16 = d_pad % 16 == 0 &&
+                    (bk_env == 16 || (bk_env == 0 && dtype == EXEM_F64));
+  if (dtype == EXEM_F32 && bk16) {
+    size_t smem = sizeof(SimtSmem<float, 16>);
+    cudaError_t e = cudaFuncSetAttribute(
+        gains_simt_kernel<float, 2, 16>,
+        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess)
+      return fail(EXEM_ERR_CUDA, "gains_simt smem: %s", cudaGetErrorString(e));
+    gains_simt_kernel<float, 2, 16><<<grid, kThreads, smem, st>>>(
+        (const float *)cvt, ldc, cnorms, l, (const float *)vt, ld, norms,
+        (const float *)m, n, d_pad, split_pts, partial);
+    EXEM_LAUNCH_CHECK("gains_simt_kernel<f32,16>");
+  } else if (dtype == EXEM_F64 && bk16) {
+    size_t smem = sizeof(SimtSmem<double, 16>);
+    cudaError_t e = cudaFuncSetAttribute(
+        gains_simt_kernel<double, 1, 16>,
+        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess)
+      return fail(EXEM_ERR_CUDA, "gains_simt smem: %s", cudaGetErrorString(e));
+    gains_simt_kernel<double, 1, 16><<<grid, kThreads, smem, st>>>(
+        (const double *)cvt, ldc, cnorms, l, (const double *)vt, ld, norms,
+        (const double *)m, n, d_pad, split_pts, partial);
+    EXEM_LAUNCH_CHECK("gains_simt_kernel<f64,16>");
+  } else if (dtype == EXEM_F32) {
     size_t smem = sizeof(SimtSmem<float>);
     gains_simt_kernel<float, 2><<<grid, kThreads, smem, st>>>(
         (const float *)cvt, ldc, cnorms, l, (const float *)vt, ld, norms,
