@@ -261,7 +261,8 @@ def test_greedy_select_all_and_tiny_shapes():
 
 
 # ------------------------------------------------------------------ SIMT gains
-@pytest.mark.parametrize("prec,n,d", [(P32, 20_000, 100), (P64, 6000, 16), (P32, 5000, 2)])
+@pytest.mark.parametrize("prec,n,d", [(P32, 20_000, 100), (P64, 6000, 16), (P32, 5000, 2),
+                                      (P64, 2500, 48)])
 def test_greedy_simt_matches_fp64_truth(prec, n, d):
     """K3-SIMT gains and the whole Greedy trajectory vs the fp64 oracle in
     the incremental form on the same (storage-rounded) inputs."""
