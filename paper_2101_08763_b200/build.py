@@ -37,8 +37,20 @@ def _nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
+STAMP = PKG / "_build" / "flags.txt"  # extra flags of the library on disk
+
+
+def _extra_flags() -> list:
+    return os.environ.get("EXEM_NVCC_FLAGS", "").split()  # experiments
+
+
 def _stale() -> bool:
     if not LIB.exists():
+        return True
+    # a probe / trace build (EXEM_NVCC_FLAGS) is never reused as the shipped
+    # library, and vice versa
+    built = STAMP.read_text().split() if STAMP.exists() else None
+    if built != _extra_flags():
         return True
     t = LIB.stat().st_mtime
     return any(p.stat().st_mtime > t for p in SOURCES + HEADERS)
@@ -54,8 +66,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     objs = []
     for src in SOURCES:
         obj = build_dir / (src.stem + ".o")
-        extra = os.environ.get("EXEM_NVCC_FLAGS", "").split()  # experiments
-        cmd = [nvcc, *NVCC_FLAGS, *extra, "-c", str(src), "-o", str(obj)]
+        cmd = [nvcc, *NVCC_FLAGS, *_extra_flags(), "-c", str(src), "-o",
+               str(obj)]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.run(cmd, check=True)
@@ -67,6 +79,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)
     os.replace(tmp, LIB)
+    STAMP.write_text(" ".join(_extra_flags()))
     return LIB
 
 
