@@ -37,7 +37,9 @@ def _nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-STAMP = PKG / "_build" / "flags.txt"  # extra flags of the library on disk
+# extra nvcc flags of the library on disk (travels with the .so to the GPU
+# box; _build/ does not)
+STAMP = PKG / "libexem_b200.so.flags"
 
 
 def _extra_flags() -> list:
@@ -79,7 +81,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)
     os.replace(tmp, LIB)
-    STAMP.write_text(" ".join(_extra_flags()))
+    STAMP.write_text(" ".join(_extra_flags()) + "\n")
     return LIB
 
 
