@@ -28,7 +28,7 @@ single GPU for any number of ranks.
 from __future__ import annotations
 
 from dataclasses import dataclass
-from typing import Optional, Protocol
+from typing import Protocol
 
 import numpy as np
 
@@ -114,7 +114,7 @@ def build_sharded_ground(V: np.ndarray, precision, rank: int, world: int,
                          device=None, aux="zero") -> ShardedGround:
     """Upload V, build the candidate replica and this rank's point shard."""
     from . import _native as N
-    from .core import _aux_vector, build_ground_set
+    from .core import build_ground_set
     from .device import prepare_ground
 
     full = build_ground_set(V, aux=aux, precision=precision, device=device)

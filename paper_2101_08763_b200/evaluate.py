@@ -28,7 +28,6 @@ from .core import (
     PackedBatch,
     Precision,
     compute_kernel_config,
-    pack_batch,
 )
 from .errors import DimensionMismatchError, OutOfMemoryError
 from .objective import (
