@@ -65,15 +65,18 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     build_dir = PKG / "_build"
     build_dir.mkdir(exist_ok=True)
     nvcc = _nvcc()
-    objs = []
-    for src in SOURCES:
+    objs, procs = [], []
+    for src in SOURCES:  # the translation units compile in parallel
         obj = build_dir / (src.stem + ".o")
         cmd = [nvcc, *NVCC_FLAGS, *_extra_flags(), "-c", str(src), "-o",
                str(obj)]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
-        subprocess.run(cmd, check=True)
+        procs.append((cmd, subprocess.Popen(cmd)))
         objs.append(str(obj))
+    failed = [cmd for cmd, p in procs if p.wait() != 0]
+    if failed:
+        raise subprocess.CalledProcessError(1, failed[0])
     tmp = LIB.with_suffix(".so.tmp")
     cmd = [nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a",
            *objs, "-o", str(tmp), "-cudart", "static"]

@@ -105,6 +105,31 @@ template <> __device__ __forceinline__ double tinf<double>() {
   return __longlong_as_double(0x7ff0000000000000ll);
 }
 
+// ------------------------------------------- folded constant columns (TC)
+// A per-row constant t >= 0 (h = (||v||^2 - m)/2 or b = ||c||^2/2) rides in
+// three storage-type pieces that the other operand multiplies by its "ones"
+// columns [kFoldScale, 1, 1]:  t = p0*kFoldScale + p1 + p2.  binary16 tops
+// out at 65504, so its first piece is t / 2^11 (exact power-of-two scale;
+// t up to 1.3e8, i.e. ||v||^2 < 2.6e8, checked on the host before the TC
+// path is chosen); the residues stay below 2^15.  bfloat16 has the fp32
+// range and keeps the scale at 1.
+template <typename S> struct FoldScale { static constexpr double v = 1.0; };
+template <> struct FoldScale<__half> { static constexpr double v = 2048.0; };
+
+template <typename S>
+__device__ __forceinline__ void fold_pieces(double t, double (&p)[3]) {
+  constexpr double sc = FoldScale<S>::v;
+  p[0] = (double)to_c(from_d<S>(t / sc));
+  const double r1 = t - p[0] * sc;
+  p[1] = (double)to_c(from_d<S>(r1));
+  p[2] = (double)to_c(from_d<S>(r1 - p[1]));
+}
+// value of ones column `piece` (0..2) of the opposite operand
+template <typename S>
+__device__ __forceinline__ double fold_one(int piece) {
+  return piece == 0 ? FoldScale<S>::v : 1.0;
+}
+
 // Distance in the reference's per-precision form.
 //  GEMM form (f32/f64, objective.py:83-89): out=-2x; out+=b2; out+=e2; max 0
 template <typename T>

@@ -426,7 +426,9 @@ __global__ void __launch_bounds__(kRedThreads)
   const int64_t c = sel_idx[step];
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   double v = 0.0;
-  if (i < n) {
+  if (i < n && c < 0) {  // K5 found no valid candidate: S unchanged
+    v = (double)m[i];
+  } else if (i < n) {
     C acc = C(0);
     int kk = 0;
     for (; kk + kLoadAhead <= d; kk += kLoadAhead) {  // loads ahead (MLP)
@@ -463,15 +465,12 @@ __global__ void __launch_bounds__(kRedThreads)
     v = (double)mi;
     if (xp != nullptr) {
       // h_i = (||v_i||^2 - m_i)/2 split into three half pieces (~24 bits).
-      double h = 0.5 * (norms[i] - (double)mi);
-      S h0 = from_d<S>(h);
-      double r1 = h - (double)to_c(h0);
-      S h1 = from_d<S>(r1);
-      S h2 = from_d<S>(r1 - (double)to_c(h1));
+      double h[3];
+      fold_pieces<S>(0.5 * (norms[i] - (double)mi), h);
       S *row = xp + i * kp + d;
-      row[0] = from_d<S>(-(double)to_c(h0));
-      row[1] = from_d<S>(-(double)to_c(h1));
-      row[2] = from_d<S>(-(double)to_c(h2));
+      row[0] = from_d<S>(-h[0]);
+      row[1] = from_d<S>(-h[1]);
+      row[2] = from_d<S>(-h[2]);
     }
   }
   double r = block_sum<kRedThreads>(v, sh);
@@ -819,11 +818,18 @@ __global__ void __launch_bounds__(kArgThreads)
                        (int64_t)__double_as_longlong(scratch[2 * b + 1])});
   x = block_best(x);
   if (threadIdx.x == 0) {
-    int64_t j = x.i;
-    if (j == INT64_MAX) j = 0;  // unreachable for k <= n (optimize.py:47-50)
-    selected[j] = 1;
-    sel_idx[step] = index_map ? index_map[j] : j;
-    sel_gain[step] = x.v;
+    const int64_t j = x.i;
+    if (j == INT64_MAX) {
+      // no valid candidate (every gain NaN or already selected): sentinel
+      // -1, which K2 treats as "S unchanged" and the host turns into an
+      // error (never a silent duplicate exemplar)
+      sel_idx[step] = -1;
+      sel_gain[step] = x.v;
+    } else {
+      selected[j] = 1;
+      sel_idx[step] = index_map ? index_map[j] : j;
+      sel_gain[step] = x.v;
+    }
   }
 }
 

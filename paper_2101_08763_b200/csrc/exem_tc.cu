@@ -629,15 +629,13 @@ __global__ void pack_kernel(const float *__restrict__ vt, int64_t ld,
         const int c = k - d;
         const bool ones = kCand ? (c < 3) : (c >= 3);
         if (ones) {
-          v = 1.0;
+          v = fold_one<S>(kCand ? c : c - 3);
         } else {
           const double t = kCand ? 0.5 * norms[r]
                                  : 0.5 * (norms[r] - (m ? (double)m[r] : 0.0));
-          const double t0 = (double)to_c(from_d<S>(t));
-          const double t1 = (double)to_c(from_d<S>(t - t0));
-          const double t2 = (double)to_c(from_d<S>(t - t0 - t1));
-          const int piece = kCand ? c - 3 : c;
-          v = -(piece == 0 ? t0 : (piece == 1 ? t1 : t2));
+          double p[3];
+          fold_pieces<S>(t, p);
+          v = -p[kCand ? c - 3 : c];
         }
       }
     }

@@ -719,14 +719,11 @@ __global__ void pack_sets_kernel(const float *__restrict__ packed,
       if (k < d) {
         v = (double)packed[(int64_t)k * ldp + (int64_t)src * l_pad + j];
       } else if (k < d + 3) {
-        v = 1.0;
+        v = fold_one<S>(k - d);
       } else if (k < d + kTcConst) {
-        const double t = 0.5 * pnorms[(int64_t)src * l_pad + j];
-        const double t0 = (double)to_c(from_d<S>(t));
-        const double t1 = (double)to_c(from_d<S>(t - t0));
-        const double t2 = (double)to_c(from_d<S>(t - t0 - t1));
-        const int piece = k - d - 3;
-        v = -(piece == 0 ? t0 : (piece == 1 ? t1 : t2));
+        double p[3];
+        fold_pieces<S>(0.5 * pnorms[(int64_t)src * l_pad + j], p);
+        v = -p[k - d - 3];
       }
     }
     x[r * kp + k] = from_d<S>(v);

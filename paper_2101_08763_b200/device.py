@@ -91,6 +91,29 @@ def padded_rows(rows: np.ndarray, d_pad: int, precision, dev):
     return t.from_numpy(host).to(dev)
 
 
+# binary16 tensor-core operands carry ||x||^2/2 folded into three f16 pieces
+# p0*2^11 + p1 + p2 (fold_pieces, exem_common.cuh) with p0 <= 65504.
+F16_FOLD_MAX_NORM = 2.0 * 65504.0 * 2048.0
+
+
+def fold_ok(precision, max_norm) -> bool:
+    """Whether norms up to ``max_norm`` fit the folded tensor-core operands
+    of ``precision`` (only binary16 has a range limit).  Beyond it the
+    binary16 paths run on the CUDA cores (K3-SIMT / K4), which use the
+    reference's direct form and have no such limit."""
+    return precision.tag != N.F16 or float(max_norm) < F16_FOLD_MAX_NORM
+
+
+def ground_fold_ok(ground, device=None) -> bool:
+    """``fold_ok`` for a ground set, resident or streamed (the streamed
+    build records the largest ||v||^2 it saw)."""
+    if ground.precision.tag != N.F16:
+        return True
+    if ground.streamed:
+        return fold_ok(ground.precision, ground._ext()["max_norm"])
+    return device_ground(ground, device).fold_ok()
+
+
 class DeviceGround:
     """Device layouts of one ground set on one CUDA device."""
 
@@ -114,6 +137,32 @@ class DeviceGround:
         self._xc = None
         self._xp0 = None
         self.kp = int(lib.tc_kp(self.d)) if precision.is_half else 0
+        self._max_norm = None
+
+    def column_major_storage(self) -> np.ndarray:
+        """(n, d) column-major host array of the STORED values (the
+        reference's GroundSet.matrix layout), read back from ``vt``: exact,
+        since vt holds the storage values widened to the compute type."""
+        t = torch()
+        tag = self.precision.tag
+        with t.cuda.device(self.device_index):
+            v = self.vt[: self.d, : self.n]
+            if tag == N.BF16:
+                host = v.to(t.bfloat16).view(t.int16).cpu().numpy().view(
+                    self.precision.dtype)
+            elif tag == N.F16:
+                host = v.to(t.float16).cpu().numpy()
+            else:
+                host = v.contiguous().cpu().numpy()
+        return host.T  # (d, n) C-order == (n, d) F-order
+
+    def fold_ok(self) -> bool:
+        """Folded tensor-core operands are valid for this ground set."""
+        if self.precision.tag != N.F16:
+            return True
+        if self._max_norm is None:
+            self._max_norm = float(self.norms[: self.n].max().item())
+        return fold_ok(self.precision, self._max_norm)
 
     @property
     def stream(self):

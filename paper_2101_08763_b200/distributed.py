@@ -98,11 +98,58 @@ class DeviceShardOps:
         return self.run.sel_idx.cpu().numpy()
 
 
+class EmptyShardOps:
+    """``ShardOps`` of a rank that owns no points (more ranks than splits):
+    it contributes zero gains and zero m-sums and runs the same K5 argmax on
+    the all-reduced gains, so its picks equal every other rank's."""
+
+    def __init__(self, cand, k: int):
+        from . import _native as N
+        from .device import torch
+
+        t = torch()
+        self.N, self.lib, self.cand = N, N.lib(), cand
+        dev = cand.dev
+        self.l = cand.n
+        self.gains = t.zeros(self.l, dtype=t.float64, device=dev)
+        self.selected = t.zeros(self.l, dtype=t.uint8, device=dev)
+        self.sel_idx = t.zeros(k, dtype=t.int64, device=dev)
+        self.sel_gain = t.zeros(k, dtype=t.float64, device=dev)
+        self.msum = t.zeros(k, dtype=t.float64, device=dev)
+        self.scratch = t.empty(int(self.lib.reduce_scratch(self.l)),
+                               dtype=t.float64, device=dev)
+
+    def start(self):
+        pass
+
+    def local_gains(self):
+        self.gains.zero_()
+
+    def gains_buffer(self):
+        return self.gains
+
+    def select(self, step):
+        N = self.N
+        self.lib.argmax_select(N.ptr(self.gains), self.l, N.ptr(self.selected),
+                               None, step, N.ptr(self.sel_idx),
+                               N.ptr(self.sel_gain), N.ptr(self.scratch),
+                               self.cand.stream)
+
+    def update(self, step):
+        pass
+
+    def msum_buffer(self):
+        return self.msum
+
+    def picks(self):
+        return self.sel_idx.cpu().numpy()
+
+
 @dataclass
 class ShardedGround:
     """Local shard + candidate replica of one rank."""
 
-    local: object        # DeviceGround of rows [r0, r1)
+    local: object        # DeviceGround of rows [r0, r1) (None: no rows)
     cand: object         # DeviceGround of all of V (candidates)
     rows: tuple
     n: int
@@ -123,6 +170,8 @@ def build_sharded_ground(V: np.ndarray, precision, rank: int, world: int,
     r0, r1 = shard_rows(full.n, world, rank, sp)
     if world == 1:
         local = cand
+    elif r1 <= r0:  # more ranks than splits: this rank owns no points
+        local = None
     else:
         local, _, _ = prepare_ground(full.matrix[r0:r1], full.aux,
                                      precision, device)
@@ -137,15 +186,23 @@ def sharded_greedy(sg: ShardedGround, k: int, group=None):
     from . import _native as N
     from .optimize import GreedyRun
 
+    from .device import torch
+    from .optimize import checked_picks
+
     sp = int(N.lib().split_points(sg.n))
-    run = GreedyRun(sg.local, cand=sg.cand, k_cap=k, split_pts=sp)
-    ops = DeviceShardOps(run)
 
     def all_reduce(t):
         if dist.is_available() and dist.is_initialized():
             dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
 
-    picks, msum = sharded_greedy_loop(ops, k, all_reduce)
+    with torch().cuda.device(sg.cand.device_index):
+        if sg.local is None:
+            ops = EmptyShardOps(sg.cand, k)
+        else:
+            ops = DeviceShardOps(GreedyRun(sg.local, cand=sg.cand, k_cap=k,
+                                           split_pts=sp))
+        picks, msum = sharded_greedy_loop(ops, k, all_reduce)
+        picks = checked_picks(picks, k)
     acc = sg.precision.accumulate_dtype
     ms = msum.cpu().numpy()[:k]
     vals = acc.type(sg.aux_loss) - ms.astype(acc) / acc.type(sg.n)
@@ -224,12 +281,19 @@ class PeerGains:
 
         from . import _native as N
 
-        self.lib = lib = N.lib()
+        self.lib = N.lib()
         self.l = l
         self.dev = device
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         self.group = group
+        # the IPC allocations and the flag kernel go to the current device
+        # (static cudart): make it the run's device
+        with torch.cuda.device(device):
+            self._open(ctypes, torch, dist, N)
+
+    def _open(self, ctypes, torch, dist, N):
+        lib, l, device, group = self.lib, self.l, self.dev, self.group
         ptr = ctypes.c_void_p()
         lib.ipc_alloc(2 * l * 8, ctypes.byref(ptr))
         self.own = ptr.value
@@ -306,9 +370,19 @@ def peer_greedy(sg: ShardedGround, k: int, group=None):
     import torch.distributed as dist
 
     from . import _native as N
-    from .optimize import GreedyRun
+    from .device import torch
+    from .optimize import GreedyRun, checked_picks
 
+    if sg.local is None:
+        raise ValueError(
+            "peer_greedy needs at least one split of points per rank "
+            f"(n={sg.n}); use sharded_greedy or fewer ranks")
     sp = int(N.lib().split_points(sg.n))
+    with torch().cuda.device(sg.local.device_index):
+        return _peer_greedy(sg, k, group, sp, GreedyRun, checked_picks, dist)
+
+
+def _peer_greedy(sg, k, group, sp, GreedyRun, checked_picks, dist):
     run = GreedyRun(sg.local, cand=sg.cand, k_cap=k, split_pts=sp)
     peer = PeerGains(run.l, run.dg.dev, group)
     try:
@@ -320,7 +394,7 @@ def peer_greedy(sg: ShardedGround, k: int, group=None):
             run.update(step)
         if dist.is_initialized():
             dist.all_reduce(run.msum, op=dist.ReduceOp.SUM, group=group)
-        picks = run.sel_idx.cpu().numpy()[:k]
+        picks = checked_picks(run.sel_idx.cpu().numpy(), k)
         msum = run.msum.cpu().numpy()[:k]
     finally:
         peer.close()

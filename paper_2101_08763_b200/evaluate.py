@@ -147,7 +147,7 @@ class DeviceBatch:
 
     def __init__(self, values: Optional[np.ndarray], d: int, k_max: int,
                  l: int, cardinalities, precision: Precision, d_pad: int, dev,
-                 stream, sets=None):
+                 stream, sets=None, ground_fold_ok: bool = True):
         """``values``: a packed (d, k_max, l) host buffer (PackedBatch), or
         None with ``sets`` = the l element arrays, which are concatenated on
         the host and interleaved on the device (exem_pack_elements)."""
@@ -188,7 +188,17 @@ class DeviceBatch:
                              device=dev)
         self.xs = None
         self.bs = None
-        if tc_batch_supported(precision, k_max):
+        use_tc = tc_batch_supported(precision, k_max)
+        if use_tc and precision.tag == N.F16:
+            # binary16 operands: every norm must be in the folded range (the
+            # same rule for the plain layout, whose fp32 GEMM form cancels
+            # catastrophically at such norms; the CUDA-core K4 uses the
+            # reference's direct form)
+            from .device import fold_ok
+
+            use_tc = ground_fold_ok and (l == 0 or fold_ok(
+                precision, self.pnorms.max().item()))
+        if use_tc:
             rows = int(lib.tc_set_rows(l, k_max))
             tdt = t.bfloat16 if precision.tag == N.BF16 else t.float16
             self.xs = t.empty((rows, int(lib.tc_batch_kp(d))), dtype=tdt,
@@ -242,7 +252,8 @@ def device_packed_sums(ground: GroundSet, values: Optional[np.ndarray],
     with t.cuda.device(dg.device_index):
         st = dg.stream
         batch = DeviceBatch(values, d, k_max, l, cardinalities,
-                            ground.precision, dg.d_pad, dg.dev, st, sets=sets)
+                            ground.precision, dg.d_pad, dg.dev, st, sets=sets,
+                            ground_fold_ok=dg.fold_ok())
         partial = t.empty((dg.splits, l), dtype=t.float64, device=dg.dev)
         batch_partials(dg, batch, partial, dg.split_pts, dg.splits)
         sums = t.empty(l, dtype=t.float64, device=dg.dev)

@@ -31,6 +31,7 @@ from .errors import (
     BudgetExceedsGroundSetError,
     EmptyEvaluationSetError,
     InstanceTooLargeError,
+    InvalidDataError,
 )
 from .evaluate import (
     Evaluator,
@@ -79,6 +80,8 @@ class GreedyRun:
         self.cand = cand or dg
         self.prec = dg.precision
         self.tc = self.prec.is_half if tc is None else tc
+        if self.tc and not (dg.fold_ok() and self.cand.fold_ok()):
+            raise_fold_range(self.prec)
         # binary32 gains on the tensor cores through split-bf16 operands
         # (exem_tc_pack_split): the K3-TC kernel with d' = 6d
         # (d <= 128: beyond, the tensor core's fp32 accumulation over
@@ -198,6 +201,32 @@ class GreedyRun:
         self.update(step)
 
 
+def raise_fold_range(precision) -> None:
+    """Greedy runs half precisions on the tensor cores only; binary16 norms
+    beyond the folded operand range (device.F16_FOLD_MAX_NORM) cannot be
+    represented there."""
+    from .device import F16_FOLD_MAX_NORM
+
+    raise InvalidDataError(
+        f"{precision.name} Greedy: squared norms reach beyond "
+        f"{F16_FOLD_MAX_NORM:.3g}, the range of the binary16 tensor-core "
+        "operands; use Precision.binary32 (evaluate_single / evaluate_batch "
+        "handle such data at binary16 on the CUDA cores)")
+
+
+def checked_picks(idx: np.ndarray, k: int) -> np.ndarray:
+    """The first k device picks; K5 writes -1 when a step had no valid
+    candidate (every remaining gain NaN), which is an error here rather than
+    a silent duplicate exemplar."""
+    idx = np.asarray(idx)[:k]
+    bad = np.flatnonzero(idx < 0)
+    if bad.size:
+        raise InvalidDataError(
+            f"greedy step {int(bad[0])} found no valid candidate "
+            "(every remaining marginal gain is NaN)")
+    return idx
+
+
 def _chunk_for_budget(ground: GroundSet, step: int, budget: Optional[int]):
     """Candidate chunk size under the reference's mu_s rule (or None)."""
     if budget is None:
@@ -236,7 +265,7 @@ def greedy_maximize(ground: GroundSet, k: int,
 
         idx, msum = stream_greedy(ground, k, evaluator.device)
         return OptimizationResult(
-            exemplar_indices=tuple(int(i) for i in idx[:k]),
+            exemplar_indices=tuple(int(i) for i in checked_picks(idx, k)),
             values=trajectory_values(ground, msum[:k]),
             evaluations=sum(ground.n - i for i in range(k)),
         )
@@ -251,7 +280,7 @@ def greedy_maximize(ground: GroundSet, k: int,
         idx = run.sel_idx.cpu().numpy()
         msum = run.msum.cpu().numpy()
     return OptimizationResult(
-        exemplar_indices=tuple(int(i) for i in idx[:k]),
+        exemplar_indices=tuple(int(i) for i in checked_picks(idx, k)),
         values=trajectory_values(ground, msum[:k]),
         evaluations=sum(ground.n - i for i in range(k)),
     )

@@ -291,14 +291,20 @@ def stream_build(ground, free_bytes: int, device=None,
             cdt = t.float64 if ground.precision.compute_dtype == np.float64 \
                 else t.float32
             host_aux = t.empty(ground.n, dtype=cdt, pin_memory=True)
+            f16 = ground.precision.tag == N.F16
+            max_norm = t.zeros((), dtype=t.float64, device=gs.dev)
             for slot, r0, r1 in gs.slices(pack_points=False):
                 host_aux[r0:r1].copy_(slot.aux[: r1 - r0], non_blocking=True)
+                if f16:  # range of the folded tensor-core operands
+                    t.maximum(max_norm, slot.norms[: r1 - r0].max(),
+                              out=max_norm)
             total = t.empty(1, dtype=t.float64, device=gs.dev)
             count = -(-int(gs.lib.pad_points(ground.n)) // 256)
             gs.lib.sum_fixed(N.ptr(gs.block_partials), count, N.ptr(total), 0,
                              N.stream_handle(gs.dev))
             t.cuda.synchronize(gs.dev)
             aux = host_aux.numpy().astype(aux_dtype(ground.precision))
+            ground._ext()["max_norm"] = float(max_norm.item())
             return aux, float(total.item())
     finally:
         gs.close()
@@ -366,7 +372,7 @@ def stream_packed_sums(ground, values, d, k_max, l, cardinalities,
     device tensor), the per-split partials are written there at their
     global split rows and no reduction is done (the sharded caller reduces
     after its collective)."""
-    from .device import torch
+    from .device import ground_fold_ok, torch
     from .evaluate import DeviceBatch, batch_partials
 
     t = torch()
@@ -382,7 +388,8 @@ def stream_packed_sums(ground, values, d, k_max, l, cardinalities,
         with t.cuda.device(gs.idx):
             st = N.stream_handle(gs.dev)
             batch = DeviceBatch(values, d, k_max, l, cardinalities, prec,
-                                int(lib.pad_dims(d)), gs.dev, st, sets=sets)
+                                int(lib.pad_dims(d)), gs.dev, st, sets=sets,
+                                ground_fold_ok=ground_fold_ok(ground))
             own = partial is None
             if own:
                 partial = t.zeros((splits, l), dtype=t.float64, device=gs.dev)
@@ -416,7 +423,8 @@ def stream_greedy(ground, k: int, device=None):
     run.  Everything is bit-identical to the resident Greedy.  Returns
     (indices, msum) as host arrays.
     """
-    from .device import compute_torch_dtype, padded_rows, to_device_bytes, torch
+    from .device import (compute_torch_dtype, ground_fold_ok, padded_rows,
+                         to_device_bytes, torch)
 
     t = torch()
     lib = N.lib()
@@ -426,6 +434,10 @@ def stream_greedy(ground, k: int, device=None):
     splits = -(-n // sp)
     cs = _csize(prec)
     half = prec.is_half
+    if half and not ground_fold_ok(ground):
+        from .optimize import raise_fold_range
+
+        raise_fold_range(prec)
     budget = ground.device_budget
     state = n * cs + n + 8 * n + 3 * 8 * k + _margin(n) + \
         int(lib.reduce_scratch(max(n, 1))) * 8
@@ -535,6 +547,10 @@ def stream_greedy(ground, k: int, device=None):
                                   N.ptr(sel_idx), N.ptr(sel_gain),
                                   N.ptr(scratch), st)
                 c = int(sel_idx[step].item())
+                if c < 0:
+                    from .optimize import checked_picks
+
+                    checked_picks(sel_idx[: step + 1].cpu().numpy(), step + 1)
                 row = padded_rows(ground.matrix[c:c + 1], d_pad, prec, dev)
                 chosen[:, 0].copy_(row[0])
                 lib.row_norms(prec.tag, N.ptr(row), 1, d, d_pad, N.ptr(cnorm),

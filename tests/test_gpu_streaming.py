@@ -130,12 +130,15 @@ def test_streamed_greedy_matches_resident(prec):
 
 @pytest.mark.parametrize("prec", [P32, P64, BF16, P16])
 def test_row_major_input_matches_column_major(prec):
-    """A C-order input is uploaded untransposed and K1's row-major variant
-    (exem_ground_prepare_rows) transposes on the device; everything derived
-    from it -- aux distances, L({e0}), batch sums, Greedy -- is bit-identical
-    to the column-major (reference layout) path, resident and streamed."""
+    """A large C-order input is uploaded untransposed and K1's row-major
+    variant (exem_ground_prepare_rows) transposes on the device (resident;
+    streamed ground sets transpose on the host); GroundSet.matrix is
+    column-major either way, and everything derived from it -- aux
+    distances, L({e0}), batch sums, Greedy -- is bit-identical to the
+    column-major (reference layout) path, resident and streamed."""
     rng = np.random.default_rng(5)
-    n, d, l, k = 20_003, 45, 40, 3
+    n, d, l, k = 30_003, 45, 40, 3
+    assert n * d >= 1 << 20  # the device-transpose size class
     data = rng.standard_normal((n, d)) * (0.5 if prec is P16 else 1.0)
     rows = np.ascontiguousarray(data.astype(prec.dtype))
     cols = np.asfortranarray(rows)
@@ -146,7 +149,8 @@ def test_row_major_input_matches_column_major(prec):
     for src in (cols, rows):
         for kw in ({}, {"device_budget": budget}):
             g = pb.build_ground_set(src, precision=prec, **kw)
-            assert g.matrix.flags.c_contiguous == (src is rows)
+            assert g.matrix.flags.f_contiguous
+            assert np.array_equal(g.matrix, rows)
             b = EvaluationBatch.from_sets([g.matrix[i] for i in idx])
             got = (g.aux_loss, g.aux_distances.copy(),
                    pb.evaluate_batch(Evaluator(), g, b),

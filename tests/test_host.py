@@ -300,3 +300,23 @@ def test_tc_set_geometry(native_lib):
         assert rows == -(-1000 // spt.value) * nc.value
     spt, w, nc = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
     assert geo(257, ctypes.byref(spt), ctypes.byref(w), ctypes.byref(nc)) == 5
+
+
+def test_groundset_fields_match_reference():
+    """Same dataclass fields as the reference's GroundSet (core.py:127-143);
+    device state lives outside the fields."""
+    import dataclasses
+
+    import paper_2101_08763_b200 as pb
+
+    names = [f.name for f in dataclasses.fields(pb.GroundSet)]
+    assert names == ["matrix", "precision", "aux", "aux_distances", "aux_loss"]
+
+
+def test_checked_picks_sentinel():
+    from paper_2101_08763_b200.errors import InvalidDataError
+    from paper_2101_08763_b200.optimize import checked_picks
+
+    assert list(checked_picks(np.array([4, 2, 9]), 2)) == [4, 2]
+    with pytest.raises(InvalidDataError):
+        checked_picks(np.array([4, -1, 9]), 3)
