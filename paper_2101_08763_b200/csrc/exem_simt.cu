@@ -887,28 +887,74 @@ __global__ void __launch_bounds__(kArgThreads)
 }
 
 // ============================================================ distances
+// out[i][j] = d(a_i, b_j), the reference's per-precision form
+// (objective.py:75-90).  64 x 64 output tile per CTA, 256 threads with 4 x 4
+// outputs each; k-chunks of 16 staged through shared memory so every a / b
+// element is read from global memory once per tile (not once per output);
+// per output the k-sum runs sequentially with fma, as before tiling.
+constexpr int kDistTile = 64, kDistK = 16;
 template <int DT>
-__global__ void distance_matrix_kernel(const typename Traits<DT>::C *a,
-                                       const double *an, int64_t m,
-                                       const typename Traits<DT>::C *b,
-                                       const double *bn, int64_t q, int d,
-                                       int64_t d_pad,
-                                       typename Traits<DT>::C *out) {
+__global__ void __launch_bounds__(256)
+    distance_matrix_kernel(const typename Traits<DT>::C *__restrict__ a,
+                           const double *__restrict__ an, int64_t m,
+                           const typename Traits<DT>::C *__restrict__ b,
+                           const double *__restrict__ bn, int64_t q, int d,
+                           int64_t d_pad, typename Traits<DT>::C *out) {
   using C = typename Traits<DT>::C;
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= m * q) return;
-  const int64_t i = idx / q, j = idx % q;
-  C acc = C(0);
-  for (int k = 0; k < d; ++k) {
-    const C x = a[i * d_pad + k], y = b[j * d_pad + k];
-    if (Traits<DT>::kDirect) {
-      const C df = x - y;
-      acc = fma(df, df, acc);
-    } else {
-      acc = fma(x, y, acc);
+  __shared__ C sa[kDistK][kDistTile + 1];
+  __shared__ C sb[kDistK][kDistTile + 1];
+  const int64_t i0 = (int64_t)blockIdx.y * kDistTile;
+  const int64_t j0 = (int64_t)blockIdx.x * kDistTile;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  C acc[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) acc[u][v] = C(0);
+  for (int k0 = 0; k0 < d; k0 += kDistK) {
+    // consecutive threads read consecutive k of one row (rows are d_pad
+    // long, zero padded): 16-element runs
+    for (int e = threadIdx.x; e < kDistTile * kDistK; e += 256) {
+      const int r = e / kDistK, kk = e % kDistK, k = k0 + kk;
+      const int64_t gi = i0 + r, gj = j0 + r;
+      sa[kk][r] = (gi < m && k < d_pad) ? a[gi * d_pad + k] : C(0);
+      sb[kk][r] = (gj < q && k < d_pad) ? b[gj * d_pad + k] : C(0);
+    }
+    __syncthreads();
+    const int kn = min(kDistK, d - k0);
+    for (int kk = 0; kk < kn; ++kk) {
+      C av[4], bv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) av[u] = sa[kk][ty + 16 * u];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) bv[v] = sb[kk][tx + 16 * v];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          if (Traits<DT>::kDirect) {
+            const C df = av[u] - bv[v];
+            acc[u][v] = fma(df, df, acc[u][v]);
+          } else {
+            acc[u][v] = fma(av[u], bv[v], acc[u][v]);
+          }
+        }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int64_t i = i0 + ty + 16 * u;
+    if (i >= m) continue;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int64_t j = j0 + tx + 16 * v;
+      if (j >= q) continue;
+      out[i * q + j] = Traits<DT>::kDirect
+                           ? acc[u][v]
+                           : gemm_form<C>(acc[u][v], (C)an[i], (C)bn[j]);
     }
   }
-  out[idx] = Traits<DT>::kDirect ? acc : gemm_form<C>(acc, (C)an[i], (C)bn[j]);
 }
 
 template <typename C>
@@ -1372,10 +1418,16 @@ int exem_distance_matrix(int dtype, const void *a, const double *anorms,
   if (total == 0) return EXEM_OK;
   EXEM_DISPATCH(dtype, DT, {
     using C = typename Traits<DT>::C;
-    distance_matrix_kernel<DT><<<(unsigned)ceil_div(total, 256), 256, 0, st>>>(
-        (const C *)a, anorms, m, (const C *)b, bnorms, q, (int)d, d_pad,
-        (C *)out);
-    EXEM_LAUNCH_CHECK("distance_matrix_kernel");
+    const int64_t rows_per = (int64_t)65535 * kDistTile;  // grid.y limit
+    for (int64_t r0 = 0; r0 < m; r0 += rows_per) {
+      const int64_t mr = m - r0 < rows_per ? m - r0 : rows_per;
+      const dim3 grid((unsigned)ceil_div(q, kDistTile),
+                      (unsigned)ceil_div(mr, kDistTile));
+      distance_matrix_kernel<DT><<<grid, 256, 0, st>>>(
+          (const C *)a + r0 * d_pad, anorms + r0, mr, (const C *)b, bnorms, q,
+          (int)d, d_pad, (C *)out + r0 * q);
+      EXEM_LAUNCH_CHECK("distance_matrix_kernel");
+    }
   });
   return EXEM_OK;
 }

@@ -2,9 +2,10 @@
 
 Half-precision batches (binary16 / bfloat16, k_max <= 256) are evaluated on
 tensor cores.  Compared with the fp64 oracle on the identical half-rounded
-inputs (the parity contract of SURVEY.md 8(c) for the half paths):
+inputs (the parity contract of SURVEY.md 8(c) for the half paths, stated in
+tests/contract.py):
 
-    |L_dev - L_ref| <= 2e-4 * max(1, |L_ref|),   L = aux_loss - f
+    |f_dev - f_ref| <= HALF_F_REL * max(1, |f_ref|) + 2 ulp32(aux_loss)
 
 and the reference's own half bound (5e-2 vs binary32) through
 test_gpu_parity.py.  Geometry cases cover: one set per tile (k_max = 256),
@@ -22,6 +23,7 @@ import exem_oracle as O
 import paper_2101_08763_b200 as pb
 from paper_2101_08763_b200 import EvaluationBatch, Evaluator, Precision
 from paper_2101_08763_b200 import evaluate as E
+from contract import check_half_values, oracle_on_device_inputs
 
 pytestmark = pytest.mark.gpu
 
@@ -38,17 +40,12 @@ def _case(prec, n, d, l, kmin, kmax, seed):
     return g, sets
 
 
-def _check(g, sets, vals, nref=None):
-    x = g.matrix.astype(np.float64)
-    og = O.Ground(x, np.float64)
+def _check(g, sets, vals, nref=None, label="K4-TC"):
+    og = oracle_on_device_inputs(g)
     sub = sets if nref is None else sets[:nref]
     ref = O.evaluate_batch(og, [og.matrix[i] for i in sub])
-    got = np.asarray(vals[:len(sub)], np.float64)
-    L_dev = g.aux_loss - got
-    L_ref = og.aux_loss - ref
-    err = np.abs(L_dev - L_ref)
-    bound = 2e-4 * np.maximum(np.abs(L_ref), 1.0)
-    assert np.all(err <= bound), (err.max(), (err / bound).max())
+    check_half_values(g, vals[:len(sub)], ref,
+                      label=f"{label} {g.precision.name} n={g.n} d={g.d}")
 
 
 @pytest.mark.parametrize("prec", [BF16, P16])
