@@ -4,8 +4,11 @@
 
 One "step" is one Greedy iteration over l = n - t candidate sets S u {c}
 (kernel K3 over every candidate, K6 reduce, K5 argmax, K2 m-update).  The
-run is one Greedy of k = W + K steps: the first W steps are untimed warm-up,
-the next K are timed (default 3 + 47 = 50 = BASELINE's k).  N > 1 runs under
+device run is one Greedy of W + K steps: the first W steps are untimed
+warm-up, the next K are timed (default 3 + 47 = 50 = BASELINE's k); the e2e
+leg always runs the full k = 50 Greedy through the public API.  Unless
+--no-sub, the other BASELINE configs follow as sub-records ("configs",
+tools/bench_configs.py: C2, C3, C5 and the other C4 precisions).  N > 1 runs under
 torchrun: V is row-sharded, the l partial gains are all-reduced over NCCL
 each step (strong scaling: the problem is fixed, N GPUs share it).
 
@@ -57,7 +60,13 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-sub", action="store_true",
+                    help="skip the other BASELINE configs (sub-records)")
+    ap.add_argument("--sub-cpu-seconds", type=float, default=2.0)
     return ap.parse_args()
+
+
+K_FULL = 50  # BASELINE config 4: Greedy k = 50
 
 
 def synthetic(n, d, seed):
@@ -165,8 +174,11 @@ def run_reference(args, rank, world):
     per_step = max(1.0, min(args.cpu_seconds / 4, 4.0))
     for step in range(args.warmup):  # untimed: worker pool, page-in of V
         cpu_sample(n, d, args.seed + step, step + 1, 0.25, threads, V)
-    for step in range(args.warmup, args.warmup + args.steps):
-        set_size = step + 1  # Greedy step t evaluates |S u {c}| = t+1
+    for i, step in enumerate(range(args.warmup, args.warmup + args.steps)):
+        # the timed steps sample the set sizes of the whole k = 50 Greedy
+        # (|S u {c}| = 1..50): the CPU's per-set cost grows with |S|, the
+        # device's per-step cost does not
+        set_size = 1 + int(round(i * (K_FULL - 1) / max(1, args.steps - 1)))
         rate, cnt, t = cpu_sample(n, d, args.seed + step, set_size, per_step,
                                   threads, V)
         total_sets += cnt
@@ -181,13 +193,13 @@ def run_reference(args, rank, world):
         f"{args.seed}",
         "config": {"workload": "C4 Greedy n=1M d=100 k=50 (CPU port of the "
                    "reference, bounded sample per step)", "n": n, "d": d,
-                   "k": args.warmup + args.steps},
+                   "k": K_FULL},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads,
                          "kind": "port",
-                         "sample": f"{total_sets} sets of size t+1 at steps "
-                         f"{args.warmup}..{args.warmup + args.steps - 1}, "
-                         "full n, numpy/OpenBLAS restatement, 1 BLAS thread "
-                         "per worker"},
+                         "sample": f"{total_sets} sets, sizes spread over "
+                         f"1..{K_FULL} (the whole k={K_FULL} Greedy) across "
+                         f"the {args.steps} steps, full n, numpy/OpenBLAS "
+                         "restatement, 1 BLAS thread per worker"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -350,13 +362,14 @@ def main():
         cpu = None
         if not args.no_cpu and world >= 1:
             threads = os.cpu_count() or 1
-            mid = (args.warmup + k) // 2 + 1
+            mid = (K_FULL + 1) // 2 + 1  # mean |S u c| of the k=50 Greedy
             rate, cnt, secs = cpu_sample(n, d, args.seed, mid, args.cpu_seconds,
                                          threads, V)
             cpu = {"value": rate, "unit": UNIT, "cores": threads,
                    "kind": "port",
                    "sample": f"{cnt} sets of size {mid} (mean |S u c| of the "
-                   f"timed steps) at full n={n}, d={d}, fp32, {secs:.1f}s; "
+                   f"k={K_FULL} Greedy) at full n={n}, d={d}, fp32, "
+                   f"{secs:.1f}s; "
                    "oracle/exem_oracle.py numpy/OpenBLAS restatement of "
                    "evaluate.py:142-170"}
         clocks = clk.summary()
@@ -374,7 +387,10 @@ def main():
                        "candidate sets S u {c} (K3 gains + K6 + K5 argmax + "
                        "K2 m-update)" + (" [fp32 gains on tensor cores, "
                                          "split-bf16]" if run.split32 else ""),
-                       "n": n, "d": d, "k": k,
+                       "n": n, "d": d, "k": K_FULL,
+                       "device_timed_steps": f"{args.warmup}..{k - 1} of a "
+                       f"{k}-step run (per-step work depends only on "
+                       "l = n - t); e2e runs the full k",
                        "parallelism": f"row-shard x{world}" if world > 1 else
                        "1 GPU", "l2": "inputs larger than L2 (V operands "
                        f"{2 * n * 128 * 2 / 2**20:.0f} MiB)"},
@@ -400,21 +416,28 @@ def main():
         del run, ops, sg
         torch.cuda.empty_cache()
         torch.cuda.synchronize()
+        ke = max(K_FULL, k)  # the full k = 50 Greedy through the public API
         t_start = time.perf_counter()
         g = pb.build_ground_set(V, precision=prec)
         res = pb.greedy_maximize(
-            g, k=k, evaluator=pb.Evaluator(tensor_fp32=args.tensor_fp32))
+            g, k=ke, evaluator=pb.Evaluator(tensor_fp32=args.tensor_fp32))
         t_e2e = time.perf_counter() - t_start
-        e2e_evals = float(sum(n - t for t in range(k)))
-        h2d = n * d * prec.bytes_per_value + d * prec.bytes_per_value
-        d2h = n * np.dtype(np.float32).itemsize + 2 * 8 * k + 8
+        e2e_evals = float(sum(n - t for t in range(ke)))
+        # H2D: V (storage dtype, row-major as generated) + e0; D2H: the
+        # column-major GroundSet.matrix (transposed on the device), the
+        # aux distances, aux sum, picks and trajectory sums
+        vb = n * d * prec.bytes_per_value
+        h2d = vb + d * prec.bytes_per_value
+        d2h = vb + n * np.dtype(np.float32).itemsize + 2 * 8 * ke + 8
         result["e2e"] = {"value": e2e_evals / t_e2e, "unit": UNIT,
-                         "h2d_bytes_per_step": h2d / k,
-                         "d2h_bytes_per_step": d2h / k,
-                         "seconds": t_e2e, "steps": k,
-                         "api": "build_ground_set(numpy) + greedy_maximize(k)",
+                         "h2d_bytes_per_step": h2d / ke,
+                         "d2h_bytes_per_step": d2h / ke,
+                         "seconds": t_e2e, "steps": ke,
+                         "api": "build_ground_set(numpy C-order float32) + "
+                                f"greedy_maximize(k={ke})",
                          "picks_match_device_run":
-                         list(res.exemplar_indices) == [int(x) for x in picks]}
+                         list(res.exemplar_indices[:k]) ==
+                         [int(x) for x in picks]}
     elif world > 1 and not args.no_e2e:
         # e2e through the public multi-GPU API: every rank uploads V from host
         # memory (build_sharded_ground: candidate replica + its row shard) and
@@ -449,6 +472,17 @@ def main():
     elif rank == 0:
         result["e2e"] = {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0,
                          "d2h_bytes_per_step": 0, "note": "--no-e2e"}
+    if rank == 0 and world == 1 and not args.no_sub:
+        # the other BASELINE configs, a few steps each (tools/bench_configs)
+        sys.path.insert(0, str(ROOT / "tools"))
+        import bench_configs
+
+        torch.cuda.empty_cache()
+        with ClockSampler(local) as clk2:
+            result["configs"] = bench_configs.all_records(
+                cpu_seconds=args.sub_cpu_seconds,
+                headline_precision=args.precision, log=sys.stderr)
+        result["configs_clocks"] = clk2.summary()
     if rank == 0:
         print(json.dumps(result), flush=True)
     if world > 1:

@@ -195,6 +195,14 @@ class GreedyRun:
                                   N.ptr(self.xp), self.kp, self.tc_d,
                                   self.stream)
 
+    def force(self, step: int, index: int):
+        """Teacher forcing: take ``index`` as the exemplar of ``step``
+        (instead of K5's argmax), then K2 as usual.  No gains are needed
+        for a forced step."""
+        self.sel_idx[step] = int(index)
+        self.selected[int(index)] = 1
+        self.update(step)
+
     def step(self, step: int, chunk: Optional[int] = None):
         self.compute_gains(chunk)
         self.select(step)

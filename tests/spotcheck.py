@@ -91,11 +91,9 @@ def device_greedy_with_checks(g, k: int, check_steps, n_random: int = 16,
                              "G_dev": G[cands], "top": top})
             if forced is None:
                 run.select(step)
+                run.update(step)
             else:
-                c = int(forced[step])
-                run.sel_idx[step] = c
-                run.selected[c] = 1
-            run.update(step)
+                run.force(step, int(forced[step]))
         picks = run.sel_idx.cpu().numpy()[:k].tolist()
         msum = run.msum.cpu().numpy()[:k]
     return picks, list(trajectory_values(g, msum)), caps

@@ -26,11 +26,11 @@ if want bench; then
 fi
 if want ncu; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
-    --log-file "$OUT/launches.csv" python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu \
+    --log-file "$OUT/launches.csv" python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu --no-sub \
     > "$OUT/ncu_launches.log" 2>&1
   echo "ncu launches rc=$?"
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:gains_tc \
-    -s 1 -c 1 -o "$OUT/prof_gains_tc" -f python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu \
+    -s 1 -c 1 -o "$OUT/prof_gains_tc" -f python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu --no-sub \
     > "$OUT/ncu_full.log" 2>&1
   echo "ncu full rc=$?"; tail -3 "$OUT/ncu_full.log"
 fi
