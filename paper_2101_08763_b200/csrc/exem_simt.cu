@@ -214,125 +214,228 @@ __global__ void __launch_bounds__(kRedThreads)
 }
 
 // ============================================================ K2 set_min
-// One thread per point; the set's elements are staged through shared memory
-// in chunks of kSetChunk rows and each thread keeps kSetChunk dot products in
-// registers, so V is streamed ceil(k / kSetChunk) times (HBM-bound).
-constexpr int kSetChunk = 8;
-constexpr int kLoadAhead = 8;  // independent V loads in flight per thread
+// min_distances / _set_value / assign_clusters over ONE explicit set
+// (objective.py:113-141, evaluate.py:105-112, optimize.py:115-136).
+//
+// One pass over V for up to KG set elements (64 at f32, 32 at f64; larger
+// sets take ceil(k / KG) passes): a CTA owns 256 points; V streams through a
+// 4-stage cp.async ring in 8-dimension chunks ([8][256] values, 16-byte
+// copies) together with the matching [8][KG] slice of the elements
+// (transposed on the fly by 4/8-byte copies, zero-filled past k), and every
+// thread keeps a 4-point x KG/4-element block of dot products in registers
+// (register-blocked outer product: one 16-byte shared load of 4 points and
+// KG/16 vector loads of elements per 4*KG/4 FMAs).  Per point the distances
+// use the reference's per-precision form, the minimum keeps the lowest
+// element index on ties (strict <, then the lowest index across the four
+// element lanes), and the per-256-point block partial of sum_i t_i is the
+// same fixed-order block_sum as every other K1/K2 kernel.  Each distance is
+// the same sequential fma chain over the dimensions as before tiling.
+//
+// Algorithmic bytes: n * d * 4 (f32 vt) read once + the elements from L2.
+constexpr int kLoadAhead = 8;  // independent V loads in flight (K2 update)
+constexpr int kSmP = 256;      // points per CTA
+constexpr int kSmBK = 8;       // dimensions per ring stage (= kDimPad)
+constexpr int kSmStages = 4;
 
-template <int DT, int CH>
-__global__ void __launch_bounds__(kRedThreads)
+template <typename C> struct SmVec;
+template <> struct SmVec<float> { using V = float4; };
+template <> struct SmVec<double> { using V = double2; };
+
+__device__ __forceinline__ void cp_async_small(void *smem, const void *gmem,
+                                               int bytes, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const int src = valid ? bytes : 0;  // 0: zero fill
+  if (bytes == 4)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s),
+                 "l"(gmem), "r"(src));
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s),
+                 "l"(gmem), "r"(src));
+}
+
+template <int DT, int KG>
+__global__ void __launch_bounds__(kRedThreads, DT == EXEM_F64 ? 1 : 2)
     set_min_kernel(const typename Traits<DT>::C *__restrict__ vt, int64_t ld,
-                   int64_t n, int d, const double *__restrict__ norms,
+                   int64_t n, int d_pad, const double *__restrict__ norms,
                    const typename Traits<DT>::C *__restrict__ aux,
-                   const typename Traits<DT>::C *__restrict__ elems, int d_pad,
+                   const typename Traits<DT>::C *__restrict__ elems,
                    const double *__restrict__ enorms, int k, int include_aux,
                    typename Traits<DT>::C *__restrict__ t_out,
                    int64_t *__restrict__ label_out,
                    double *__restrict__ partials,
-                   typename Traits<DT>::C *__restrict__ dist_out = nullptr,
-                   int64_t ldd = 0) {
+                   typename Traits<DT>::C *__restrict__ dist_out, int64_t ldd) {
   using C = typename Traits<DT>::C;
+  using V4 = typename SmVec<C>::V;
+  constexpr int EPT = KG / 4;                   // elements per thread
+  constexpr int VPER = 16 / sizeof(C);          // values per 16-byte vector
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  C *se = reinterpret_cast<C *>(smem_raw);  // [CH][d_pad]
+  C *sv = reinterpret_cast<C *>(smem_raw);                  // [ST][BK][P]
+  C *se = sv + kSmStages * kSmBK * kSmP;                    // [ST][BK][KG]
   __shared__ double sh[32];
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool live = i < n;
-  const C ai = live ? (C)norms[i] : C(0);
-  C best = tinf<C>();
-  int64_t lab = 0;
-  for (int e0 = 0; e0 < k; e0 += CH) {
-    const int ec = min(CH, k - e0);
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < ec * d_pad; idx += blockDim.x)
-      se[idx] = elems[(int64_t)e0 * d_pad + idx];
-    __syncthreads();
-    C acc[CH];
+  __shared__ C st_t[kSmP];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int te = lane & 3;                      // element lane
+  const int tp = warp * 8 + (lane >> 2);        // point quad 0..63
+  const int64_t i0 = (int64_t)blockIdx.x * kSmP;
+  const int nc = d_pad / kSmBK;
+  C best[4];
+  int64_t lab[4];
 #pragma unroll
-    for (int e = 0; e < CH; ++e) acc[e] = C(0);
-    if (live) {
-      // HBM-bound: issue kLoadAhead independent coalesced loads per thread
-      // before using them (memory-level parallelism), then the FMAs
-      int kk = 0;
-      for (; kk + kLoadAhead <= d; kk += kLoadAhead) {
-        C xs[kLoadAhead];
+  for (int p = 0; p < 4; ++p) {
+    best[p] = tinf<C>();
+    lab[p] = 0;
+  }
+  for (int g0 = 0; g0 < k; g0 += KG) {
+    auto load = [&](int stage, int chunk) {
+      C *dv = sv + stage * kSmBK * kSmP;
+      C *de = se + stage * kSmBK * KG;
+      constexpr int VG = kSmBK * kSmP / VPER;  // 16-byte granules of V
+      for (int x = threadIdx.x; x < VG; x += kRedThreads) {
+        const int r = x / (kSmP / VPER), c = (x % (kSmP / VPER)) * VPER;
+        cp_async16(dv + r * kSmP + c,
+                   vt + (int64_t)(chunk * kSmBK + r) * ld + i0 + c);
+      }
+      for (int x = threadIdx.x; x < kSmBK * KG; x += kRedThreads) {
+        const int r = x / KG, e = x % KG;
+        const bool ok = g0 + e < k;
+        cp_async_small(de + r * KG + e,
+                       elems + (int64_t)(ok ? g0 + e : 0) * d_pad +
+                           chunk * kSmBK + r,
+                       (int)sizeof(C), ok);
+      }
+    };
+    C acc[4][EPT];
 #pragma unroll
-        for (int u = 0; u < kLoadAhead; ++u)
-          xs[u] = vt[(int64_t)(kk + u) * ld + i];
+    for (int p = 0; p < 4; ++p)
 #pragma unroll
-        for (int u = 0; u < kLoadAhead; ++u)
+      for (int j = 0; j < EPT; ++j) acc[p][j] = C(0);
+    __syncthreads();  // the previous group's ring is fully consumed
 #pragma unroll
-          for (int e = 0; e < CH; ++e) {
+    for (int s = 0; s < kSmStages - 1; ++s) {
+      if (s < nc) load(s, s);
+      cp_async_commit();
+    }
+    for (int c = 0; c < nc; ++c) {
+      cp_async_wait<kSmStages - 2>();
+      __syncthreads();
+      const int cn = c + kSmStages - 1;
+      if (cn < nc) load(cn % kSmStages, cn);
+      cp_async_commit();
+      const C *cv = sv + (c % kSmStages) * kSmBK * kSmP + tp * 4;
+      const C *ce = se + (c % kSmStages) * kSmBK * KG + te * EPT;
+#pragma unroll
+      for (int kk = 0; kk < kSmBK; ++kk) {
+        C pv[4], ev[EPT];
+        if constexpr (sizeof(C) == 4) {
+          const float4 q = *reinterpret_cast<const float4 *>(cv + kk * kSmP);
+          pv[0] = q.x; pv[1] = q.y; pv[2] = q.z; pv[3] = q.w;
+        } else {
+          const V4 q0 = *reinterpret_cast<const V4 *>(cv + kk * kSmP);
+          const V4 q1 = *reinterpret_cast<const V4 *>(cv + kk * kSmP + 2);
+          pv[0] = q0.x; pv[1] = q0.y; pv[2] = q1.x; pv[3] = q1.y;
+        }
+        if constexpr (EPT * sizeof(C) % 16 == 0) {
+#pragma unroll
+          for (int j = 0; j < EPT; j += VPER) {
+            const V4 q = *reinterpret_cast<const V4 *>(ce + kk * KG + j);
+            const C *qc = reinterpret_cast<const C *>(&q);
+#pragma unroll
+            for (int u = 0; u < VPER; ++u) ev[j + u] = qc[u];
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < EPT; ++j) ev[j] = ce[kk * KG + j];
+        }
+#pragma unroll
+        for (int p = 0; p < 4; ++p)
+#pragma unroll
+          for (int j = 0; j < EPT; ++j) {
             if (Traits<DT>::kDirect) {
-              const C df = xs[u] - se[e * d_pad + kk + u];
-              acc[e] = fma(df, df, acc[e]);
+              const C df = pv[p] - ev[j];
+              acc[p][j] = fma(df, df, acc[p][j]);
             } else {
-              acc[e] = fma(xs[u], se[e * d_pad + kk + u], acc[e]);
+              acc[p][j] = fma(pv[p], ev[j], acc[p][j]);
             }
           }
       }
-      for (; kk < d; ++kk) {
-        const C x = vt[(int64_t)kk * ld + i];
+    }
+    cp_async_wait<0>();
+    // epilogue of the group: distances, running first minimum per point
 #pragma unroll
-        for (int e = 0; e < CH; ++e) {
-          if (Traits<DT>::kDirect) {
-            const C df = x - se[e * d_pad + kk];
-            acc[e] = fma(df, df, acc[e]);
-          } else {
-            acc[e] = fma(x, se[e * d_pad + kk], acc[e]);
-          }
-        }
-      }
+    for (int p = 0; p < 4; ++p) {
+      const int64_t i = i0 + tp * 4 + p;
+      const C ai = i < n ? (C)norms[i] : C(0);
 #pragma unroll
-      for (int e = 0; e < CH; ++e) {
-        if (e < ec) {
-          C dist = Traits<DT>::kDirect
-                       ? acc[e]
-                       : gemm_form<C>(acc[e], ai, (C)enorms[e0 + e]);
-          if (dist_out) dist_out[(int64_t)(e0 + e) * ldd + i] = dist;
-          if (dist < best) {  // strict: lowest element index wins ties
-            best = dist;
-            lab = e0 + e;
+      for (int j = 0; j < EPT; ++j) {
+        const int e = g0 + te * EPT + j;
+        if (e < k && i < n) {
+          const C dist = Traits<DT>::kDirect
+                             ? acc[p][j]
+                             : gemm_form<C>(acc[p][j], ai, (C)enorms[e]);
+          if (dist_out) dist_out[(int64_t)e * ldd + i] = dist;
+          if (dist < best[p]) {  // strict: lowest element index wins ties
+            best[p] = dist;
+            lab[p] = e;
           }
         }
       }
     }
   }
-  C t = best;
-  if (include_aux && live) t = tmin(t, aux[i]);
-  if (live) {
-    if (t_out) t_out[i] = t;
-    if (label_out) label_out[i] = lab;
+  // first minimum across the four element lanes (lower index on ties)
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+#pragma unroll
+    for (int o = 1; o < 4; o <<= 1) {
+      const C ob = __shfl_xor_sync(0xffffffffu, best[p], o);
+      const long long ol = __shfl_xor_sync(0xffffffffu, (long long)lab[p], o);
+      if (ob < best[p] || (ob == best[p] && ol < lab[p])) {
+        best[p] = ob;
+        lab[p] = ol;
+      }
+    }
+    const int64_t i = i0 + tp * 4 + p;
+    C t = best[p];
+    if (include_aux && i < n) t = tmin(t, aux[i]);
+    if (te == 0) {
+      st_t[tp * 4 + p] = t;
+      if (i < n) {
+        if (t_out) t_out[i] = t;
+        if (label_out) label_out[i] = lab[p];
+      }
+    }
   }
-  double r = block_sum<kRedThreads>(live ? (double)t : 0.0, sh);
+  __syncthreads();
+  const int64_t i = i0 + threadIdx.x;
+  double r = block_sum<kRedThreads>(i < n ? (double)st_t[threadIdx.x] : 0.0,
+                                    sh);
   if (threadIdx.x == 0) partials[blockIdx.x] = r;
 }
 
-// Element chunk CH = the smallest of 1, 2, 4, 8 covering k (k < 8 computes
-// no dead dot products); the per-element accumulation order is the same for
-// every CH, so the distances are identical.
-template <int DT, int CH>
-static cudaError_t launch_set_min_ch(
+template <int DT, int KG>
+static cudaError_t launch_set_min_kg(
     int64_t blocks, cudaStream_t st, const typename Traits<DT>::C *vt,
-    int64_t ld, int64_t n, int d, const double *norms,
+    int64_t ld, int64_t n, int d_pad, const double *norms,
     const typename Traits<DT>::C *aux, const typename Traits<DT>::C *elems,
-    int d_pad, const double *enorms, int k, int include_aux,
+    const double *enorms, int k, int include_aux,
     typename Traits<DT>::C *t_out, int64_t *label_out, double *partials,
     typename Traits<DT>::C *dist_out, int64_t ldd) {
   using C = typename Traits<DT>::C;
-  const size_t smem = (size_t)CH * d_pad * sizeof(C);
+  const size_t smem = (size_t)kSmStages * kSmBK * (kSmP + KG) * sizeof(C);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(
-        set_min_kernel<DT, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        set_min_kernel<DT, KG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
         (int)smem);
     if (e != cudaSuccess) return e;
   }
-  set_min_kernel<DT, CH><<<(unsigned)blocks, kRedThreads, smem, st>>>(
-      vt, ld, n, d, norms, aux, elems, d_pad, enorms, k, include_aux, t_out,
+  set_min_kernel<DT, KG><<<(unsigned)blocks, kRedThreads, smem, st>>>(
+      vt, ld, n, d_pad, norms, aux, elems, enorms, k, include_aux, t_out,
       label_out, partials, dist_out, ldd);
   return cudaGetLastError();
 }
 
+// Element group KG = the smallest of 8, 16, 32, 64 (32 at f64) covering k:
+// small sets compute few dead dot products; the per-element arithmetic is
+// the same for every KG, so the distances are identical.
 template <int DT>
 static cudaError_t launch_set_min(
     int64_t blocks, cudaStream_t st, const typename Traits<DT>::C *vt,
@@ -341,14 +444,19 @@ static cudaError_t launch_set_min(
     int d_pad, const double *enorms, int k, int include_aux,
     typename Traits<DT>::C *t_out, int64_t *label_out, double *partials,
     typename Traits<DT>::C *dist_out = nullptr, int64_t ldd = 0) {
-#define EXEM_SM(CHN)                                                        \
-  return launch_set_min_ch<DT, CHN>(blocks, st, vt, ld, n, d, norms, aux,   \
-                                    elems, d_pad, enorms, k, include_aux,   \
-                                    t_out, label_out, partials, dist_out, ldd)
-  if (k >= 8) EXEM_SM(8);
-  if (k >= 4) EXEM_SM(4);
-  if (k >= 2) EXEM_SM(2);
-  EXEM_SM(1);
+  (void)d;
+  if (ld % kSmP != 0 || d_pad % kSmBK != 0) return cudaErrorInvalidValue;
+#define EXEM_SM(KGN)                                                        \
+  return launch_set_min_kg<DT, KGN>(blocks, st, vt, ld, n, d_pad, norms,    \
+                                    aux, elems, enorms, k, include_aux,     \
+                                    t_out, label_out, partials, dist_out,   \
+                                    ldd)
+  if constexpr (DT != EXEM_F64) {
+    if (k > 32) EXEM_SM(64);
+  }
+  if (k > 16) EXEM_SM(32);
+  if (k > 8) EXEM_SM(16);
+  EXEM_SM(8);
 #undef EXEM_SM
 }
 
