@@ -57,6 +57,9 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--tensor-fp32", action="store_true",
                     help="fp32 gains on tensor cores via split-bf16 operands")
+    ap.add_argument("--graph", action="store_true",
+                    help="replay the timed steps from one CUDA graph "
+                    "(optimize.capture_steps; NCCL all-reduce captured too)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
@@ -223,7 +226,9 @@ def main():
     import paper_2101_08763_b200 as pb
     from paper_2101_08763_b200 import _native as N
     from paper_2101_08763_b200.distributed import (DeviceShardOps,
-                                                   build_sharded_ground)
+                                                   build_sharded_ground,
+                                                   communicator_record,
+                                                   pin_nccl_env)
     from paper_2101_08763_b200.optimize import GreedyRun
 
     # EXEM_BENCH_SHARE_GPU=1 (testing only): every rank on cuda:0 over gloo,
@@ -237,8 +242,13 @@ def main():
         if share:
             dist.init_process_group("gloo")
         else:
+            pin_nccl_env()  # fixed algo/proto; INIT log (nRanks) on stderr
             dist.init_process_group("nccl",
                                     device_id=torch.device("cuda", local))
+        comm = communicator_record()
+        if rank == 0:
+            print(f"communicator: {json.dumps(comm)}", file=sys.stderr,
+                  flush=True)
     prec = pb.Precision.from_name(args.precision)
     n, d = args.n, args.d
     k = args.warmup + args.steps
@@ -265,11 +275,13 @@ def main():
     orig = run.compute_gains
 
     def timed_gains(chunk=None, out=None):
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        a.record(stream)
+        # external events: recorded as graph nodes under --graph capture
+        cur = torch.cuda.current_stream()
+        a = torch.cuda.Event(enable_timing=True, external=args.graph)
+        b = torch.cuda.Event(enable_timing=True, external=args.graph)
+        a.record(cur)
         orig(chunk, out=out)
-        b.record(stream)
+        b.record(cur)
         ev.append((a, b))
 
     # EXEM_PEER_REDUCE=1 (N > 1): per-step exchange over CUDA-IPC peer memory
@@ -299,18 +311,31 @@ def main():
     barrier()
     run.compute_gains = timed_gains
     launches0 = lib.launch_count()
+    graph = None
+    if args.graph:
+        from paper_2101_08763_b200.optimize import capture_steps
+
+        graph = capture_steps(range(args.warmup, k), do_step)
+        captured = lib.launch_count() - launches0
+        torch.cuda.synchronize()
+        barrier()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         barrier()
         t0.record(stream)
-        for step in range(args.warmup, k):
-            do_step(step)
+        if graph is not None:
+            graph.replay()
+        else:
+            for step in range(args.warmup, k):
+                do_step(step)
         t1.record(stream)
         torch.cuda.synchronize()
         barrier()
-    launches = lib.launch_count() - launches0
+    # kernels launched in the timed region (a replay runs the captured ones)
+    launches = (captured if graph is not None
+                else lib.launch_count() - launches0)
     ms_local = t0.elapsed_time(t1)
     run.compute_gains = orig
     if peer is not None:
@@ -380,6 +405,7 @@ def main():
             "vs_baseline": None, "dtype": args.precision,
             "data": f"synthetic Gaussian N(0,1) float32 seed {args.seed}, "
                     f"stored as {args.precision}",
+            "communicator": comm if world > 1 else None,
             "exchange": "peer memory (CUDA IPC, fused sum+argmax)" if peer
             is not None else (f"{dist.get_backend()} all-reduce" if world > 1
                               else "none"),
@@ -408,6 +434,7 @@ def main():
                          "kernel_share_of_step": gains_ms_local * args.steps / ms},
             "cpu_baseline": cpu,
             "gpu_launches": int(launches),
+            "cuda_graph": bool(args.graph),
             "clocks": clocks,
             "picks_head": [int(x) for x in picks[:5]],
         }

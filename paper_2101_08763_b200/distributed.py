@@ -33,6 +33,54 @@ from typing import Protocol
 import numpy as np
 
 
+# NCCL settings applied before the communicator is created (SURVEY.md 8(e)
+# "Determinism"): a fixed algorithm and protocol make the summation order of
+# the per-step all-reduce -- and so every fp64 gain bit -- repeatable run to
+# run for a given rank count (NCCL otherwise tunes per message size and
+# topology).  Ring/Simple moves the 8 MB gains vector in ~10-30 us on NVLink
+# 5, < 0.1 % of a step.  The INIT log (one line per rank with "nRanks") goes
+# to stderr so a scaling run can verify the communicator size without
+# touching the JSON line on stdout.  Every setting is a default only: an
+# explicit environment value wins.
+NCCL_DEFAULTS = {
+    "NCCL_ALGO": "Ring",
+    "NCCL_PROTO": "Simple",
+    "NCCL_DEBUG": "INFO",
+    "NCCL_DEBUG_SUBSYS": "INIT",
+    "NCCL_DEBUG_FILE": "/dev/stderr",
+}
+
+
+def pin_nccl_env(environ=None) -> dict:
+    """Apply ``NCCL_DEFAULTS`` (setdefault) and return the effective values;
+    call before ``init_process_group("nccl")``."""
+    import os
+
+    env = os.environ if environ is None else environ
+    for key, val in NCCL_DEFAULTS.items():
+        env.setdefault(key, val)
+    return {k: env[k] for k in ("NCCL_ALGO", "NCCL_PROTO")}
+
+
+def communicator_record(group=None) -> dict:
+    """What a scaling run must be able to check: ranks, backend, NCCL
+    version, pinned algorithm/protocol."""
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    rec = {"backend": dist.get_backend(group),
+           "nranks": dist.get_world_size(group),
+           "nccl_algo": os.environ.get("NCCL_ALGO"),
+           "nccl_proto": os.environ.get("NCCL_PROTO")}
+    try:
+        rec["nccl_version"] = ".".join(str(x) for x in torch.cuda.nccl.version())
+    except Exception:  # noqa: BLE001 -- no NCCL in this torch build
+        rec["nccl_version"] = None
+    return rec
+
+
 def shard_rows(n: int, world: int, rank: int, split_pts: int) -> tuple:
     """[r0, r1) rows of rank ``rank``: whole splits, as even as possible."""
     if world < 1 or not 0 <= rank < world:
@@ -66,6 +114,24 @@ def sharded_greedy_loop(ops: ShardOps, k: int, all_reduce, on_step=None):
         ops.update(step)
         if on_step is not None:
             on_step(step)
+    all_reduce(ops.msum_buffer())
+    return ops.picks()[:k], ops.msum_buffer()
+
+
+def sharded_greedy_graphed(ops: ShardOps, k: int, all_reduce):
+    """``sharded_greedy_loop`` with steps 1..k-1 replayed from one CUDA graph
+    (step 0 runs eagerly so every kernel and the communicator are warm)."""
+    from .optimize import capture_steps
+
+    def do_step(step):
+        ops.local_gains()
+        all_reduce(ops.gains_buffer())
+        ops.select(step)
+        ops.update(step)
+
+    ops.start()
+    do_step(0)
+    capture_steps(range(1, k), do_step).replay()
     all_reduce(ops.msum_buffer())
     return ops.picks()[:k], ops.msum_buffer()
 
@@ -179,8 +245,12 @@ def build_sharded_ground(V: np.ndarray, precision, rank: int, world: int,
                          aux_loss=full.aux_loss, precision=precision)
 
 
-def sharded_greedy(sg: ShardedGround, k: int, group=None):
-    """Row-sharded Greedy on the calling rank; returns (picks, values)."""
+def sharded_greedy(sg: ShardedGround, k: int, group=None, graph: bool = False):
+    """Row-sharded Greedy on the calling rank; returns (picks, values).
+
+    ``graph=True``: steps 1..k-1 (K3, K6, the NCCL all-reduce, K5, K2) are
+    captured into one CUDA graph after an eager step 0 and replayed once
+    (optimize.capture_steps)."""
     import torch.distributed as dist
 
     from . import _native as N
@@ -201,7 +271,10 @@ def sharded_greedy(sg: ShardedGround, k: int, group=None):
         else:
             ops = DeviceShardOps(GreedyRun(sg.local, cand=sg.cand, k_cap=k,
                                            split_pts=sp))
-        picks, msum = sharded_greedy_loop(ops, k, all_reduce)
+        if graph and k > 1:
+            picks, msum = sharded_greedy_graphed(ops, k, all_reduce)
+        else:
+            picks, msum = sharded_greedy_loop(ops, k, all_reduce)
         picks = checked_picks(picks, k)
     acc = sg.precision.accumulate_dtype
     ms = msum.cpu().numpy()[:k]

@@ -38,9 +38,10 @@ from .objective import (
     require_device_dissimilarity,
 )
 
-# Accepted backend names.  "b200" is the native name; the reference's names
-# (evaluate.py:42) are aliases of the same single device path.
-BACKENDS = ("b200", "reference", "parallel", "tiled")
+# Accepted backend names: the reference's (evaluate.py:42), in its order and
+# with its default, plus "b200"; every name selects the same single device
+# path, so existing ``Evaluator(backend=...)`` calls drop in unchanged.
+BACKENDS = ("reference", "parallel", "tiled", "b200")
 
 
 @dataclass(frozen=True)
@@ -51,7 +52,7 @@ class Evaluator:
     device path's tiling is fixed by the B200 kernels.
     """
 
-    backend: str = "b200"
+    backend: str = "reference"
     limits: DeviceLimits = field(default_factory=DeviceLimits)
     worker_count: int = 1
     precision: Optional[Precision] = None
@@ -59,6 +60,8 @@ class Evaluator:
     # binary32 Greedy gains on the tensor cores via split-bf16 operands
     # (opt-in; the default binary32 path is the CUDA-core K3-SIMT)
     tensor_fp32: bool = False
+    # Greedy: run the k-step loop as one CUDA graph (optimize.capture_steps)
+    cuda_graph: bool = False
 
     def __post_init__(self):
         if self.backend not in BACKENDS:

@@ -209,6 +209,29 @@ class GreedyRun:
         self.update(step)
 
 
+def capture_steps(steps, do_step):
+    """Record ``do_step(t)`` for every t in ``steps`` into ONE CUDA graph and
+    return it (``graph.replay()`` runs them).
+
+    A Greedy step is K3 -> K6 -> [all-reduce] -> K5 -> K2 with no host
+    synchronisation, and the step index only selects where K5/K2 write
+    (sel_idx[t], msum[t]), so the whole k-step loop -- including the NCCL
+    all-reduce of a row-sharded run -- is capturable: one graph launch
+    replaces ~5 launches per step and takes the host out of the loop
+    (SURVEY.md 8(e)).  Every kernel of the library launches on torch's
+    current stream, which ``torch.cuda.graph`` makes the capture stream.
+    The kernels must have run once before (module load, smem attributes).
+    """
+    from .device import torch
+
+    t = torch()
+    graph = t.cuda.CUDAGraph()
+    with t.cuda.graph(graph):
+        for step in steps:
+            do_step(step)
+    return graph
+
+
 def raise_fold_range(precision) -> None:
     """Greedy runs half precisions on the tensor cores only; binary16 norms
     beyond the folded operand range (device.F16_FOLD_MAX_NORM) cannot be
@@ -283,8 +306,16 @@ def greedy_maximize(ground: GroundSet, k: int,
     with torch().cuda.device(dg.device_index):
         run = GreedyRun(dg, k_cap=k, split32=evaluator.tensor_fp32)
         run.start()
-        for step in range(k):
-            run.step(step, _chunk_for_budget(ground, step, memory_budget))
+        chunks = [_chunk_for_budget(ground, step, memory_budget)
+                  for step in range(k)]
+        if evaluator.cuda_graph and k > 1:
+            # step 0 eagerly (loads every kernel), steps 1..k-1 as one graph
+            run.step(0, chunks[0])
+            capture_steps(range(1, k),
+                          lambda s: run.step(s, chunks[s])).replay()
+        else:
+            for step in range(k):
+                run.step(step, chunks[step])
         idx = run.sel_idx.cpu().numpy()
         msum = run.msum.cpu().numpy()
     return OptimizationResult(

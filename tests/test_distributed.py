@@ -176,3 +176,36 @@ def test_sharded_batch_partials_exact(world):
              nprocs=world, join=True)
     for rank in range(world):
         assert np.array_equal(out[rank], ref)
+
+
+def test_nccl_env_is_pinned_but_overridable():
+    """SURVEY 8(e) Determinism: a fixed NCCL algorithm/protocol, the INIT
+    log on stderr, explicit environment values win."""
+    from paper_2101_08763_b200.distributed import NCCL_DEFAULTS, pin_nccl_env
+
+    env = {"NCCL_PROTO": "LL128"}
+    eff = pin_nccl_env(env)
+    assert eff == {"NCCL_ALGO": "Ring", "NCCL_PROTO": "LL128"}
+    for key in NCCL_DEFAULTS:
+        assert key in env
+    assert env["NCCL_DEBUG_SUBSYS"] == "INIT"
+    assert env["NCCL_DEBUG_FILE"] == "/dev/stderr"
+
+
+def _comm_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2101_08763_b200.distributed import communicator_record
+
+    out[rank] = communicator_record()
+    dist.destroy_process_group()
+
+
+def test_communicator_record_reports_ranks():
+    port = _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_comm_worker, args=(2, port, out), nprocs=2, join=True)
+    assert out[0]["nranks"] == 2 and out[1]["nranks"] == 2
+    assert out[0]["backend"] == "gloo"
