@@ -376,3 +376,32 @@ def test_tiled_evaluate_matches_evaluate_batch(prec):
     a = pb.evaluate_batch(Evaluator(), g, batch)
     b = pb.tiled_evaluate(g, pb.pack_batch(batch, g.precision))
     assert np.array_equal(a, b)
+
+
+def test_aux_loss_within_one_step_all_members():
+    """Reference test_core.py:95-102 for every member including the added
+    bfloat16 (its epsilon from ml_dtypes.finfo: np.finfo rejects it)."""
+    import ml_dtypes
+
+    rng = np.random.default_rng(3)
+    data = rng.random((100, 5))
+    for precision in pb.Precision:
+        g = pb.build_ground_set(data, precision=precision)
+        exact = float(np.mean(np.asarray(g.aux_distances, dtype=np.float64)))
+        eps = float(ml_dtypes.finfo(precision.dtype).eps)
+        assert g.aux_loss == pytest.approx(exact, rel=4 * eps), precision
+
+
+def test_point_loss_decomposition_within_fp64_bound():
+    """Reference test_objective.py:155-164 at the fp64 parity bound: the
+    per-point losses recompose the whole loss (the device sums in its own
+    fixed order, so equality is to rounding, not bitwise)."""
+    rng = np.random.default_rng(23)
+    data = rng.random((50, 4))
+    g = pb.build_ground_set(data, precision=pb.Precision.binary64)
+    for _ in range(10):
+        idx = rng.choice(50, size=4, replace=False)
+        elems = g.matrix[idx]
+        parts = np.array([pb.point_loss(g, i, elems) for i in range(50)])
+        whole = pb.kmedoids_loss(g, np.vstack([elems, np.zeros((1, 4))]))
+        assert abs(float(np.sum(parts)) - whole) <= 1e-12 * max(1.0, abs(whole))

@@ -26,7 +26,34 @@ ROOT = Path(__file__).resolve().parents[1]
 SUITE = ROOT / "baseline" / "_ref" / "suite"
 
 # test id -> why the device implementation deviates
-EXPECTED_DEVIATIONS: dict = {}
+EXPECTED_DEVIATIONS = {
+    # timing criteria of the reference's HOST cost model
+    "test_acceptance::test_scaling_shape":
+        "requires runtime linear in n, l and k (R^2 >= 0.95) for each of the "
+        "three host backends at n <= 100k, l <= 4000; on the device every "
+        "point of that sweep is a few launches plus host<->device copies "
+        "(sub-millisecond to milliseconds), dominated by fixed latency, so "
+        "the fit is not linear -- the criterion describes the CPU emulation",
+    "test_acceptance::test_scaling_speedup_multicore":
+        "requires the 'parallel'/'tiled' host backends to beat 'reference' "
+        "by the host core count; here every backend name selects the same "
+        "single device path (north_star: no multi-backend dispatch), so all "
+        "three run at the same speed",
+    # the added bfloat16 member (north_star's tensor-core path)
+    "test_core.TestBuildGroundSet::test_aux_loss_is_mean_within_one_step":
+        "iterates over every Precision member and calls np.finfo(dtype); the "
+        "added bfloat16 member's dtype is ml_dtypes.bfloat16, which np.finfo "
+        "rejects ('not inexact'); the same check passes for the reference's "
+        "three members and for bfloat16 with ml_dtypes.finfo "
+        "(tests/test_gpu_parity.py::test_aux_loss_within_one_step_all_members)",
+    # summation order
+    "test_objective.TestPointLoss::test_decomposition_identity_fp64":
+        "asserts np.sum(point_loss) == kmedoids_loss bit for bit: the "
+        "reference computes both as numpy's pairwise sum of t_i/n, the device "
+        "sums t_i in its fixed-order fp64 tree and divides once; the two "
+        "agree to 1 ulp (0.23931167371106934 vs ...32), inside the fp64 "
+        "parity bound 1e-12 (test_objective.py:40-53)",
+}
 
 
 def _run_suite(tmp_path):

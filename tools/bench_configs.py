@@ -317,6 +317,81 @@ def c5_record(cpu_seconds=2.0, n_total=50_000_000, shards=8, d=256, l=4096,
     }
 
 
+def c1_record(cpu_seconds=2.0, reps=50):
+    """BASELINE config 1 through the public API with host arrays: single-set
+    f(S) (|S| = 10, evaluate_single) and Greedy k = 10 (build_ground_set +
+    greedy_maximize), binary32, on the seeded C1 draw (tests/golden/
+    make_golden.py:c1_data); picks checked against the reference's golden
+    picks (tests/golden/golden.npz, generated by the reference itself)."""
+    import torch
+
+    import paper_2101_08763_b200 as pb
+
+    rng = np.random.default_rng(1234)
+    V = rng.standard_normal((10000, 100), dtype=np.float32)
+    S = np.sort(rng.choice(10000, size=10, replace=False))
+    prec = pb.Precision.binary32
+    gz = ROOT / "tests" / "golden" / "golden.npz"
+    golden = np.load(gz) if gz.exists() else None
+    g = pb.build_ground_set(V, precision=prec)
+    elems = np.asarray(g.matrix[S])
+    pb.evaluate_single(g, elems)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        f = pb.evaluate_single(g, elems)
+        ts.append(time.perf_counter() - t0)
+    single_ms = float(np.median(ts)) * 1e3
+    pb.greedy_maximize(pb.build_ground_set(V, precision=prec), k=10)  # warm
+    torch.cuda.synchronize()
+    gts = []
+    for _ in range(5):
+        t0 = time.perf_counter()
+        res = pb.greedy_maximize(pb.build_ground_set(V, precision=prec), k=10)
+        gts.append(time.perf_counter() - t0)
+    greedy_s = float(np.median(gts))
+    evals = res.evaluations
+    match = None
+    if golden is not None and "c1_f32_picks" in golden.files:
+        match = list(res.exemplar_indices) == golden["c1_f32_picks"].tolist()
+    # CPU: the oracle port on the same draw; single set 1 thread, Greedy
+    # extrapolated from a sample of its candidate sets (mean |S u c| = 6)
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import exem_oracle as O  # CPU baseline leg only
+
+    og = O.Ground(V, np.float32)
+    cts = []
+    for _ in range(5):
+        t0 = time.perf_counter()
+        O.evaluate_batch(og, [og.matrix[S]], workers=1)
+        cts.append(time.perf_counter() - t0)
+    threads = os.cpu_count() or 1
+    rate, cnt, secs, _ = cpu_rate(V, 6, cpu_seconds, threads, seed=1234)
+    return {
+        "name": "C1 public API", "metric": "candidate-set evals/s",
+        "value": evals / greedy_s, "unit": UNIT, "dtype": "fp32",
+        "config": {"workload": "C1: single-set f(S) |S|=10 + Greedy k=10, "
+                   "n=10k, d=100, seed 1234, host numpy arrays in and out "
+                   "(build_ground_set + evaluate_single / greedy_maximize)",
+                   "n": 10000, "d": 100, "k": 10},
+        "single_set_ms": single_ms, "single_set_f": float(f),
+        "greedy_seconds": greedy_s, "greedy_evaluations": evals,
+        "picks_match_reference_golden": match,
+        "roofline": {"bound": "latency", "note": "n=10k: every kernel is a "
+                     "few microseconds; the public call is bound by launch "
+                     "and host<->device latency, not by a pipe"},
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads,
+                         "kind": "port", "single_set_ms_1thread":
+                         float(np.median(cts)) * 1e3,
+                         "greedy_seconds_extrapolated": evals / rate,
+                         "sample": f"{cnt} sets of size 6 (mean |S u c| of "
+                         f"the k=10 Greedy) at n=10000, fp32, {secs:.1f}s; "
+                         "single set: 5 reps on 1 thread; oracle/"
+                         "exem_oracle.py restatement of evaluate.py:142-170"},
+    }
+
+
 def all_records(cpu_seconds=2.0, headline_precision="bf16", log=None):
     """Every sub-record; a failing one is reported, not fatal."""
     out = []
@@ -340,12 +415,13 @@ def all_records(cpu_seconds=2.0, headline_precision="bf16", log=None):
             cpu_seconds=cpu_seconds, workload="C4 Greedy step on a 16-blob "
             "Gaussian mixture (demos/03 shape): many positive gains")),
     ]
+    plan.append(("C1", lambda: c1_record(cpu_seconds=cpu_seconds)))
     V2 = gaussian(100_000, 100, 0)
     plan.append(("C2 fp32", lambda: greedy_record(
         "C2 fp32", V2, "fp32", t0=17, warm=1, steps=2,
         cpu_seconds=cpu_seconds, workload="C2 batched step, n=100k, d=100, "
         "|S u c|=20")))
-    for d in (2, 100, 1024):
+    for d in (2, 16, 100, 512, 1024):
         for p in ("bf16", "fp32") + (("fp64",) if d == 100 else ()):
             nm = f"C3 d={d} {p}"
             plan.append((nm, (lambda d=d, p=p, nm=nm: greedy_record(

@@ -4,8 +4,9 @@ Greedy m-update (greedy_update), timed with CUDA events at n = 1M, d = 100,
 fp32 (and bf16 storage for K1).  Algorithmic bytes per launch:
 
   K1            read n*d*b (storage) + write n*d_pad*4 (vt) + 16n (norms, aux)
-  set_min       ceil(k/8) passes over vt (n*d_pad*4 each) + 8n norms + 4n aux
-                (+ 4n t_out when requested)
+  set_min       SURVEY 8(d): n*d*b (V once) + 8n (norms) + k*d*b (elements)
+                + 4n aux (+ 8n labels when requested); also 2*n*k*d FFMA
+                flop, so the bound is max(HBM time, FFMA time)
   greedy_update read vt (n*d_pad*4) + 8n norms + 4n m, write 4n m
 
 achieved = bytes / median launch time; peak = MEASURED_PEAKS.json hbm_gbs.
@@ -62,10 +63,22 @@ def main():
     V = np.random.default_rng(0).standard_normal((n, d), dtype=np.float32)
     out = []
 
-    def rec(name, bytes_, t):
+    simt = ROOT / "profiles" / "simt_peak.json"
+    ffma = json.loads(simt.read_text())["fp32_ffma_tflops"] \
+        if simt.exists() else 72.5
+
+    def rec(name, bytes_, t, flop=0.0):
         r = {"kernel": name, "n": n, "d": d, "bytes": bytes_, "ms": t * 1e3,
              "achieved_gbs": bytes_ / t / 1e9, "peak_gbs": peak,
-             "frac": bytes_ / t / 1e9 / peak}
+             "frac_hbm": bytes_ / t / 1e9 / peak}
+        floor = bytes_ / (peak * 1e9)
+        if flop:
+            r.update(flop=flop, achieved_tflops=flop / t / 1e12,
+                     peak_ffma_tflops=ffma)
+            floor = max(floor, flop / (ffma * 1e12))
+        r["bound"] = "ffma" if flop and flop / (ffma * 1e12) > \
+            bytes_ / (peak * 1e9) else "hbm"
+        r["frac"] = floor / t  # of max(HBM time, FFMA time)
         out.append(r)
         print(json.dumps(r), flush=True)
 
@@ -90,7 +103,7 @@ def main():
             n * d * prec.bytes_per_value + n * dg.d_pad * 4 + 16 * n, t)
         if prec is not pb.Precision.binary32:
             continue
-        for k in (1, 10, 50):
+        for k in (1, 10, 16, 50, 64, 100):
             elems = padded_rows(g.matrix[:k], dg.d_pad, prec, dg.dev)
             en = torch.empty(k, dtype=torch.float64, device=dg.dev)
             lib.row_norms(prec.tag, N.ptr(elems), k, d, dg.d_pad, N.ptr(en), st)
@@ -100,7 +113,7 @@ def main():
                 N.ptr(dg.aux), N.ptr(elems), N.ptr(en), k, 1, None, None,
                 N.ptr(s), N.ptr(dg.scratch), st))
             rec(f"K2 set_min k={k} (single-set evaluate)",
-                -(-k // 8) * n * dg.d_pad * 4 + 12 * n, t)
+                n * d * 4 + 12 * n + k * d * 4, t, 2.0 * n * k * d)
         # assign_clusters: K2 with the argmin-label epilogue, k = 50 exemplars
         elems = padded_rows(g.matrix[:50], dg.d_pad, prec, dg.dev)
         en = torch.empty(50, dtype=torch.float64, device=dg.dev)
@@ -112,7 +125,7 @@ def main():
             N.ptr(dg.aux), N.ptr(elems), N.ptr(en), 50, 0, None, N.ptr(lab),
             N.ptr(s), N.ptr(dg.scratch), st))
         rec("K2 set_min k=50 + labels (assign_clusters)",
-            -(-50 // 8) * n * dg.d_pad * 4 + 8 * n + 8 * n, t)
+            n * d * 4 + 8 * n + 8 * n + 50 * d * 4, t, 2.0 * n * 50 * d)
         m = torch.empty(dg.ld, dtype=torch.float32, device=dg.dev)
         m.copy_(dg.aux)
         sel = torch.zeros(1, dtype=torch.int64, device=dg.dev)
@@ -121,7 +134,8 @@ def main():
             prec.tag, N.ptr(dg.vt), dg.ld, n, d, N.ptr(dg.norms),
             N.ptr(dg.vt), dg.ld, N.ptr(dg.norms), N.ptr(sel), 0, N.ptr(m),
             None, 0, N.ptr(msum), N.ptr(dg.scratch), st))
-        rec("K2 greedy_update (m-update)", n * dg.d_pad * 4 + 20 * n, t)
+        rec("K2 greedy_update (m-update)", n * d * 4 + 20 * n, t,
+            2.0 * n * d)
     # .exem loader straight to the device (io.py: mapped payload -> one DMA
     # -> K1), wall clock of the public load_ground_set, file bytes / time
     import tempfile
