@@ -435,6 +435,9 @@ def main():
             "cpu_baseline": cpu,
             "gpu_launches": int(launches),
             "cuda_graph": bool(args.graph),
+            "k3_epilogue": ({"groups": run.epi,
+                             "screen_hit_fraction": run.hit_fraction}
+                            if run.tc else None),
             "clocks": clocks,
             "picks_head": [int(x) for x in picks[:5]],
         }

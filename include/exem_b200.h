@@ -50,7 +50,7 @@ extern "C" {
 #define EXEM_ERR_UNSUPPORTED 5 /* ExemError: no sm_100a device / bad dtype   */
 
 const char *exem_last_error(void);
-int exem_abi_version(void); /* 2: check_finite in K1, interleaved K4-TC set tiles */
+int exem_abi_version(void); /* 3: exem_greedy_gains_tc_ex (2: check_finite in K1, interleaved K4-TC set tiles) */
 
 /* Device query: SM count, compute capability, opt-in shared memory. */
 int exem_device_info(int device, int *sm_count, int *cc_major, int *cc_minor,
@@ -192,6 +192,22 @@ int exem_greedy_gains_simt(int dtype, const void *cvt, int64_t ldc,
 int exem_greedy_gains_tc(int dtype, const void *xc, int64_t l, const void *xp,
                          int64_t n, int64_t d, int64_t split_pts,
                          double *partial, int64_t splits, void *stream);
+/*
+ * Same as exem_greedy_gains_tc with the epilogue width chosen by the caller:
+ *   epi_groups   0 (default = 2), 2 or 4 warps per TMEM lane quarter (4:
+ *                faster when many (candidate, point) gains are positive,
+ *                e.g. clustered data; 2: when the sign screen skips most)
+ *   screen_hits  NULL, or a device counter that receives += the number of
+ *                (candidate row, 32-point chunk) screens that found a value
+ *                >= 0 (the relu-sum work done; lets the caller choose
+ *                epi_groups for the next steps).  Results do not depend on
+ *                epi_groups beyond fp32 summation order inside a tile.
+ */
+int exem_greedy_gains_tc_ex(int dtype, const void *xc, int64_t l,
+                            const void *xp, int64_t n, int64_t d,
+                            int64_t split_pts, double *partial, int64_t splits,
+                            int epi_groups, unsigned long long *screen_hits,
+                            void *stream);
 
 /*
  * K4-TC  batch_eval_tc -- explicit packed sets on tensor cores (bf16/f16).

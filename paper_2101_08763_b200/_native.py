@@ -9,6 +9,7 @@ A missing or unloadable library raises immediately -- there is no fallback.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from ctypes import c_double, c_int, c_int64, c_void_p
 from pathlib import Path
@@ -52,6 +53,9 @@ _SIGNATURES = {
                                        c_int64, _P, c_int64, _P]),
     "exem_greedy_gains_tc": (c_int, [c_int, _P, c_int64, _P, c_int64, c_int64,
                                      c_int64, _P, c_int64, _P]),
+    "exem_greedy_gains_tc_ex": (c_int, [c_int, _P, c_int64, _P, c_int64,
+                                        c_int64, c_int64, _P, c_int64, c_int,
+                                        _P, _P]),
     "exem_tc_pack_candidates": (c_int, [c_int, _P, c_int64, c_int64, c_int64,
                                         _P, _P, _P]),
     "exem_tc_pack_points": (c_int, [c_int, _P, c_int64, c_int64, c_int64, _P,
@@ -161,8 +165,8 @@ def raise_status(rc: int, msg: str):
 
 # Bumped whenever an entry point's signature or contract changes
 # (2: exem_ground_prepare[_rows] gained check_finite; K4-TC set tiles are
-# column-interleaved).
-ABI_VERSION = 2
+# column-interleaved; 3: exem_greedy_gains_tc_ex).
+ABI_VERSION = 3
 
 
 def load_library(path: Path | str | None = None) -> _Lib:
@@ -171,7 +175,10 @@ def load_library(path: Path | str | None = None) -> _Lib:
     with _lock:
         if _lib is not None and path is None:
             return _lib
-        p = Path(path) if path else LIB_PATH
+        # EXEM_LIB_PATH: an alternative build of the same library for A/B
+        # timing experiments (tools/); it is still the native library
+        p = Path(path) if path else Path(os.environ.get("EXEM_LIB_PATH",
+                                                        LIB_PATH))
         if not p.exists():
             raise ExemError(
                 f"native library {p} is missing; run "

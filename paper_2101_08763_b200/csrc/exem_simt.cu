@@ -213,6 +213,14 @@ __global__ void __launch_bounds__(kRedThreads)
   if (threadIdx.x == 0) partials[blockIdx.x] = r;
 }
 
+// TMA-fed persistent K2 (exem_setmin.cu): 0 launched, 1 shape not covered,
+// < 0 a CUDA error
+int set_min_tma(int dtype, const void *vt, int64_t ld, int64_t n, int d_pad,
+                const double *norms, const void *aux, const void *elems,
+                const double *enorms, int k, int include_aux, void *t_out,
+                int64_t *label_out, double *partials, void *dist_out,
+                int64_t ldd, cudaStream_t st);
+
 // ============================================================ K2 set_min
 // min_distances / _set_value / assign_clusters over ONE explicit set
 // (objective.py:113-141, evaluate.py:105-112, optimize.py:115-136).
@@ -446,6 +454,13 @@ static cudaError_t launch_set_min(
     typename Traits<DT>::C *dist_out = nullptr, int64_t ldd = 0) {
   (void)d;
   if (ld % kSmP != 0 || d_pad % kSmBK != 0) return cudaErrorInvalidValue;
+  // the TMA-fed persistent K2 (exem_setmin.cu) whenever the element group is
+  // resident in shared memory; this cp.async kernel otherwise
+  const int tma = set_min_tma(DT, vt, ld, n, d_pad, norms, aux, elems, enorms,
+                              k, include_aux, t_out, label_out, partials,
+                              dist_out, ldd, st);
+  if (tma == 0) return cudaSuccess;
+  if (tma < 0) return (cudaError_t)(-tma);
 #define EXEM_SM(KGN)                                                        \
   return launch_set_min_kg<DT, KGN>(blocks, st, vt, ld, n, d_pad, norms,    \
                                     aux, elems, enorms, k, include_aux,     \
@@ -1211,7 +1226,7 @@ using namespace exem;
 extern "C" {
 
 const char *exem_last_error(void) { return g_err; }
-int exem_abi_version(void) { return 2; }
+int exem_abi_version(void) { return 3; }
 int64_t exem_launch_count(void) {
   return (int64_t)__atomic_load_n(&g_launches, __ATOMIC_RELAXED);
 }

@@ -11,17 +11,19 @@
 //   b = ||c||^2/2, h_i = (||v_i||^2 - m_i)/2   =>   D = (m_i - d(v_i,c))/2
 //   partial[split][c] = sum_{i in split} max(0, D[c][i])   (x2 in K6)
 //
-// Roles (320 threads, 1 CTA/SM, persistent over (split, candidate tile)):
-//   warp 0      TMA producer: candidate tile (A, stationary per item) and
-//               point tiles (B, streamed per 64-wide K chunk) into 128B-
-//               swizzled smem, mbarrier complete_tx.
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer,
+// Roles (64 + 128*Q threads, 1 CTA/SM, persistent over (split, candidate
+// tile)):
+//   warps 0..4Q-1  epilogue: tcgen05.ld 32x32b -> relu-sum per
+//               candidate row in registers (fp32 per tile, fp64 across
+//               tiles), fixed-order merge of the column groups, one store
+//               per candidate.  Warp w drains TMEM lane quarter w % 4.
+//   warp kProdWarp  TMA producer: candidate tile (A, stationary per item)
+//               and point tiles (B, streamed per 64-wide K chunk) into
+//               128B-swizzled smem, mbarrier complete_tx.
+//   warp kMmaWarp   TMEM allocator + single-thread tcgen05.mma issuer,
 //               M=128 candidates x N=256 points x K=16, fp32 accum in TMEM,
 //               two accumulator buffers (2 x 256 columns) so the epilogue
 //               of tile t overlaps the MMAs of tile t+1.
-//   warps 2-9   epilogue: tcgen05.ld 32x32b -> relu-sum per candidate row
-//               in registers (fp32 per tile, fp64 across tiles), fixed-order
-//               merge of the two column halves, one store per candidate.
 #include <cstdlib>
 
 #include "exem_tc_common.cuh"
@@ -33,8 +35,26 @@ constexpr int BM = 128;            // candidates per tile (TMEM lanes)
 constexpr int BN = 256;            // points per tile (TMEM columns)
 constexpr int A_CHUNK = BM * 128;  // bytes of one A K-chunk
 constexpr int B_CHUNK = BN * 128;  // bytes of one B K-chunk
-constexpr int kThreads = 320;
-constexpr int kEpiWarps = 8;
+// Epilogue column groups Q: each TMEM lane quarter (32 candidates) is
+// drained by Q warps, each taking BN / Q columns of a tile (a template
+// parameter of the kernel; the host picks it per launch).  Q = 4 (16
+// epilogue warps, 4 per SMSP) halves each warp's drain + relu-sum chain per
+// tile: on data with many positive gains (a 16-blob mixture) that chain sets
+// the tile period and Q = 4 is 16 % faster; on data where the sign screen
+// skips almost everything (centred Gaussian) Q = 2 is 2 % faster
+// (tools/k3_ab.py).
+template <int Q> struct Epi {
+  static constexpr int kCols = BN / Q;        // accumulator columns per warp
+  static constexpr int kWarps = 4 * Q;        // epilogue warps
+  static constexpr int kThreads = 64 + 32 * kWarps;
+  // Role warps.  The SMSP arbiter favours the highest warp id, so the
+  // single MMA-issuing thread (whose every instruction is on the tensor
+  // pipe's critical path) and the TMA producer take the two highest warp
+  // ids; the epilogue warps 0..kWarps-1 keep warp % 4 = their TMEM lane
+  // quarter.
+  static constexpr int kProdWarp = kWarps;
+  static constexpr int kMmaWarp = kWarps + 1;
+};
 constexpr int kSmemBudget = 227 * 1024;
 constexpr int kBarBytes = 1024;
 constexpr int kTrace = 256;  // tiles traced on CTA 0 (EXEM_TC_TRACE)
@@ -207,19 +227,44 @@ __device__ __forceinline__ void mma_item_waits(
 
 
 
+// AND of 32 words as a balanced tree (depth 5 instead of a 31-deep chain;
+// the compiler fuses pairs of levels into 3-input LOP3s)
 __device__ __forceinline__ uint32_t and32(const uint32_t (&r)[32]) {
-  uint32_t a = r[0];
+  uint32_t a[16];
 #pragma unroll
-  for (int j = 1; j < 32; ++j) a &= r[j];
-  return a;
+  for (int j = 0; j < 16; ++j) a[j] = r[j] & r[j + 16];
+#pragma unroll
+  for (int w = 8; w > 0; w >>= 1)
+#pragma unroll
+    for (int j = 0; j < w; ++j) a[j] &= a[j + w];
+  return a[0];
 }
-// s_even += max(0, r[2j]), s_odd += max(0, r[2j+1]) in ascending j.
-__device__ __forceinline__ void relu_acc(const uint32_t (&r)[32], float &se,
-                                         float &so) {
+#ifdef EXEM_TC_RELU_FMNMX
+__device__ __forceinline__ void relu_acc_fmnmx(const uint32_t (&r)[32],
+                                               float &se, float &so) {
 #pragma unroll
   for (int j = 0; j < 32; j += 2) {
     se += fmaxf(__uint_as_float(r[j]), 0.f);
     so += fmaxf(__uint_as_float(r[j + 1]), 0.f);
+  }
+}
+#endif
+// acc.x += 2 max(0, r[2j]), acc.y += 2 max(0, r[2j+1]) in ascending j.
+// x + |x| is exactly 2 max(0, x) (0 or 2x), and one FADD2 with the |.|
+// operand modifier forms it for a register pair; a second FADD2 adds the
+// pair to the two running sums: 1 instruction per value instead of
+// FMNMX + FADD (the epilogue is issue-bound at 2 instructions per value on
+// data with many positive gains; tools/epi_probe.cu).  The doubled sums are
+// halved once (exact), so they equal the FMNMX + FADD sums bit for bit
+// unless a partial sum is subnormal.
+__device__ __forceinline__ void relu_acc(const uint32_t (&r)[32],
+                                         float2 &acc) {
+#pragma unroll
+  for (int j = 0; j < 32; j += 2) {
+    const float2 x = make_float2(__uint_as_float(r[j]),
+                                 __uint_as_float(r[j + 1]));
+    const float2 ax = make_float2(fabsf(x.x), fabsf(x.y));
+    acc = __fadd2_rn(acc, __fadd2_rn(x, ax));
   }
 }
 
@@ -253,6 +298,10 @@ struct Params {
   uint32_t idesc;
   double *partial;
   long long *trace;     // timing experiments only (EXEM_TC_TRACE)
+  // optional: += number of (candidate row, 32-point chunk) screens that
+  // found a value >= +0 (the relu-sum work actually done; the host uses it
+  // to pick the epilogue width Q for the following steps)
+  unsigned long long *hits;
 };
 
 // kCS > 1: kCS-CTA cluster; the CTAs score adjacent candidate tiles against
@@ -261,8 +310,8 @@ struct Params {
 // clock under the cap); a B stage is refilled only when every CTA's MMAs
 // released it (empty barriers count kCS, commits multicast).  map_ph: the
 // point operand with 256/kCS-row boxes.
-template <bool kAStream, int kCS>
-__global__ void __launch_bounds__(kThreads, 1)
+template <bool kAStream, int kCS, int kQ>
+__global__ void __launch_bounds__(Epi<kQ>::kThreads, 1)
     gains_tc_kernel(const __grid_constant__ CUtensorMap map_c,
                     const __grid_constant__ CUtensorMap map_p,
                     const __grid_constant__ CUtensorMap map_ph,
@@ -287,6 +336,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   double *red = (double *)(tmem_slot + 4);       // [BM] half-merge buffer
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int kEpiCols = Epi<kQ>::kCols;
+  constexpr int kEpiWarps = Epi<kQ>::kWarps;
+  constexpr int kProdWarp = Epi<kQ>::kProdWarp;
+  constexpr int kMmaWarp = Epi<kQ>::kMmaWarp;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < p.stages; ++s) {
@@ -303,7 +356,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&map_c));
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&map_p));
   }
-  if (warp == 1) {
+  if (warp == kMmaWarp) {
     asm volatile(
         "tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::
             "r"(su32(tmem_slot)));
@@ -324,7 +377,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int64_t nwork = gridDim.x / kCS;
   const int64_t items = cunits * p.splits;
 
-  if (warp == 0) {
+  if (warp == kProdWarp) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
       int stage = 0;
@@ -375,7 +428,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
     // One thread runs the whole role.  With whole-tile stages the K-steps of
     // a tile are issued back to back after a single barrier wait; the
@@ -511,13 +564,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   } else {
     // ------------------------------------------------------------ epilogue
-    const int ew = warp - 2;            // 0..7
+    const int ew = warp;                // 0..kEpiWarps-1
     const int q = warp & 3;             // TMEM lane quarter of this warp
-    const int half = ew >> 2;           // column half of the 256-wide tile
+    const int grp = ew >> 2;            // column group of the 256-wide tile
     const int row = q * 32 + lane;      // candidate row within the tile
     uint32_t buf = 0, tph = 0;  // tph: bit b = phase of buffer b
     int tile_no = 0;
-    const bool tr = (warp == 2 && lane == 0);
+    uint32_t nhit = 0;
+    const bool tr = (warp == 0 && lane == 0);
     for (int64_t it = wid; it < items; it += nwork) {
       const int64_t ct = kCS * (it % cunits) + crank;
       const int64_t sp = it / cunits;
@@ -538,22 +592,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         tph ^= 1u << buf;
         fence_after();
         const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) +
-                               (uint32_t)(buf * BN + half * 128);
-        // Drain this warp's 32x128 slice of the accumulator into registers
-        // first and release the TMEM buffer immediately, so the MMA of tile
-        // t+2 never waits on this tile's arithmetic.
-        uint32_t r0[32], r1[32], r2[32], r3[32];
-        TMEM_LD32(taddr, r0);
-        TMEM_LD32(taddr + 32, r1);
-        TMEM_LD32(taddr + 64, r2);
-        TMEM_LD32(taddr + 96, r3);
+                               (uint32_t)(buf * BN + grp * kEpiCols);
+        // Drain this warp's 32 x kEpiCols slice of the accumulator into
+        // registers first and release the TMEM buffer immediately, so the
+        // MMA of tile t+2 never waits on this tile's arithmetic.
+        uint32_t r[kEpiCols / 32][32];
+#pragma unroll
+        for (int c = 0; c < kEpiCols / 32; ++c) TMEM_LD32(taddr + 32 * c, r[c]);
         tmem_wait_ld();
         fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[buf]);
         if (tr) TR(6, tile_no);
         if (TC_PROBE(p, 1)) {  // timing experiment: no epilogue arithmetic
-          g += (double)__uint_as_float(r0[0] ^ r1[5] ^ r2[9] ^ r3[31]);
+          g += (double)__uint_as_float(r[0][0] ^ r[kEpiCols / 32 - 1][31]);
           buf ^= 1u;
           ++tile_no;
           continue;
@@ -562,35 +614,66 @@ __global__ void __launch_bounds__(kThreads, 1)
         // D >= +0, and almost every (candidate, point) pair has D < 0 (a
         // candidate helps only points closer to it than their current
         // exemplar).  AND-ing the raw bits of 32 values (LOP3, 3 inputs per
-        // op) leaves the sign bit set iff all 32 are negative, so the FMNMX +
-        // FADD work runs only for chunks that can contribute.  Skipped
-        // chunks would only have added +0, so the sums are bit-identical.
-        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-        if ((int)and32(r0) >= 0) relu_acc(r0, s0, s1);
-        if ((int)and32(r1) >= 0) relu_acc(r1, s2, s3);
-        if ((int)and32(r2) >= 0) relu_acc(r2, s0, s1);
-        if ((int)and32(r3) >= 0) relu_acc(r3, s2, s3);
-        g += (double)((s0 + s1) + (s2 + s3));
+        // op) leaves the sign bit set iff all 32 are negative, so the relu
+        // work runs only for chunks that can contribute.  Skipped chunks
+        // would only have added +0, so the sums are bit-identical.
+#ifdef EXEM_TC_RELU_FMNMX  // A/B experiment: FMNMX + FADD per value
+        float s[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int c = 0; c < kEpiCols / 32; ++c)
+          if ((int)and32(r[c]) >= 0)
+            relu_acc_fmnmx(r[c], s[2 * (c & 1)], s[2 * (c & 1) + 1]);
+        g += (double)((s[0] + s[1]) + (s[2] + s[3]));
+#else
+        // one pair of running sums per 32-column chunk (independent FADD2
+        // chains), combined in a fixed tree
+        constexpr int NC = kEpiCols / 32;
+        float2 a[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          a[c] = make_float2(0.f, 0.f);
+          if ((int)and32(r[c]) >= 0) {
+            relu_acc(r[c], a[c]);
+            ++nhit;
+          }
+        }
+        float sc[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) sc[c] = a[c].x + a[c].y;
+#pragma unroll
+        for (int w = NC / 2; w > 0; w >>= 1)
+#pragma unroll
+          for (int c = 0; c < w; ++c) sc[c] = sc[c] + sc[c + w];
+        g += (double)(sc[0] * 0.5f);
+#endif
         if (tr) TR(7, tile_no);
         ++tile_no;
         buf ^= 1u;
       }
-      // fixed-order merge of the two column halves
-      if (half == 1) red[row] = g;
-      asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
-      if (half == 0) {
-        const double tot = g + red[row];
-        const int64_t c = ct * BM + row;
-        if (c < p.l) p.partial[sp * p.l + c] = tot;
+      // fixed-order merge of the column groups: ((g0 + g1) + g2) + g3
+      // through one [BM] buffer
+#pragma unroll 1
+      for (int gq = 1; gq < kQ; ++gq) {
+        if (grp == gq) red[row] = g;
+        asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+        if (grp == 0) g += red[row];
+        asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
       }
-      asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+      if (grp == 0) {
+        const int64_t c = ct * BM + row;
+        if (c < p.l) p.partial[sp * p.l + c] = g;
+      }
+    }
+    if (p.hits) {
+      const uint32_t w = __reduce_add_sync(0xffffffffu, nhit);
+      if (lane == 0 && w) atomicAdd(p.hits, (unsigned long long)w);
     }
   }
 
   fence_before();
   __syncthreads();
   if constexpr (kCS > 1) cluster_sync();  // no multicast / commit in flight
-  if (warp == 1) {
+  if (warp == kMmaWarp) {
     fence_after();
     asm volatile(
         "tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
@@ -775,7 +858,19 @@ int exem_tc_pack_points(int dtype, const void *vt, int64_t ld, int64_t n,
 int exem_greedy_gains_tc(int dtype, const void *xc, int64_t l, const void *xp,
                          int64_t n, int64_t d, int64_t split_pts,
                          double *partial, int64_t splits, void *stream) {
+  return exem_greedy_gains_tc_ex(dtype, xc, l, xp, n, d, split_pts, partial,
+                                 splits, 0, nullptr, stream);
+}
+
+int exem_greedy_gains_tc_ex(int dtype, const void *xc, int64_t l,
+                            const void *xp, int64_t n, int64_t d,
+                            int64_t split_pts, double *partial, int64_t splits,
+                            int epi_groups, unsigned long long *screen_hits,
+                            void *stream) {
   using namespace exem::tc;
+  if (epi_groups != 0 && epi_groups != 2 && epi_groups != 4)
+    return fail(EXEM_ERR_ARG, "epi_groups must be 0 (default), 2 or 4");
+  const int q = epi_groups == 4 ? 4 : 2;
   if (dtype != EXEM_BF16 && dtype != EXEM_F16)
     return fail(EXEM_ERR_ARG, "greedy_gains_tc is bf16/f16 only");
   if (split_pts < BN || split_pts % BN)
@@ -803,6 +898,7 @@ int exem_greedy_gains_tc(int dtype, const void *xc, int64_t l, const void *xp,
   prm.kchunks = kchunks;
   prm.idesc = make_idesc(dtype == EXEM_BF16, BM, BN);
   prm.partial = partial;
+  prm.hits = screen_hits;
   {
     const char *dbg = getenv("EXEM_TC_DEBUG");
     prm.dbg = dbg ? atoi(dbg) : 0;
@@ -847,15 +943,25 @@ int exem_greedy_gains_tc(int dtype, const void *xc, int64_t l, const void *xp,
   cudaError_t e;
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute at[1];
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(q == 4 ? Epi<4>::kThreads : Epi<2>::kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
+  // one kernel instantiation per (A streamed, cluster size, Q)
+  auto pick = [&](bool as, int c) {
+#define EXEM_K3_PICK(AS, CS)                                                  \
+  (q == 4 ? gains_tc_kernel<AS, CS, 4> : gains_tc_kernel<AS, CS, 2>)
+    return as ? EXEM_K3_PICK(true, 1)
+              : (c == 4 ? EXEM_K3_PICK(false, 4)
+                        : (c == 2 ? EXEM_K3_PICK(false, 2)
+                                  : EXEM_K3_PICK(false, 1)));
+#undef EXEM_K3_PICK
+  };
+  auto kern = pick(astream, cs);
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+  if (e != cudaSuccess)
+    return fail(EXEM_ERR_CUDA, "smem attr: %s", cudaGetErrorString(e));
   if (mcast) {
-    auto kern = cs == 4 ? gains_tc_kernel<false, 4> : gains_tc_kernel<false, 2>;
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-    if (e != cudaSuccess)
-      return fail(EXEM_ERR_CUDA, "smem attr: %s", cudaGetErrorString(e));
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = cs;
     at[0].val.clusterDim.y = 1;
@@ -874,21 +980,7 @@ int exem_greedy_gains_tc(int dtype, const void *xc, int64_t l, const void *xp,
   } else {
     const int64_t items = prm.cand_tiles * splits;
     cfg.gridDim = dim3((unsigned)(items < sms ? items : sms));
-    if (astream) {
-      e = cudaFuncSetAttribute(gains_tc_kernel<true, 1>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)smem);
-      if (e == cudaSuccess)
-        e = cudaLaunchKernelEx(&cfg, gains_tc_kernel<true, 1>, mc, mp,
-                               mph, prm);
-    } else {
-      e = cudaFuncSetAttribute(gains_tc_kernel<false, 1>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)smem);
-      if (e == cudaSuccess)
-        e = cudaLaunchKernelEx(&cfg, gains_tc_kernel<false, 1>, mc, mp,
-                               mph, prm);
-    }
+    e = cudaLaunchKernelEx(&cfg, kern, mc, mp, mph, prm);
   }
   if (e != cudaSuccess)
     return fail(EXEM_ERR_CUDA, "gains_tc_kernel launch: %s",

@@ -59,7 +59,10 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t *b, uint32_t parity) {
         : "r"(a), "r"(parity)
         : "memory");
     if (ok) return;
-    __nanosleep(64);
+#ifndef EXEM_TC_SLEEP_NS
+#define EXEM_TC_SLEEP_NS 64
+#endif
+    __nanosleep(EXEM_TC_SLEEP_NS);
   }
 }
 __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map,

@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import itertools
 import math
+import os
 from dataclasses import dataclass
 from typing import Optional
 
@@ -50,6 +51,11 @@ from .objective import (
 
 BRUTE_FORCE_LIMIT = 10**6
 SPLIT32_MAX_D = 128
+# K3-TC epilogue width: after the first tensor-core gains launch of a run,
+# the fraction of (candidate row, 32-point chunk) sign screens that found a
+# positive gain decides between 2 and 4 epilogue warps per TMEM lane quarter
+# for the remaining steps (exem_greedy_gains_tc_ex).
+EPI_WIDE_THRESHOLD = 0.02
 
 
 @dataclass(frozen=True)
@@ -107,6 +113,10 @@ class GreedyRun:
         self._partial = None
         self.xp = None
         self.xc = None
+        # K3-TC epilogue width (0: not decided yet) and its screen counter
+        self.epi = 0
+        self.hit_fraction = None
+        self.hits = t.zeros(1, dtype=t.int64, device=dev)
         self.tc_tag = self.prec.tag
         self.tc_d = dg.d
         if self.split32:
@@ -160,9 +170,12 @@ class GreedyRun:
             if self.tc:
                 xc_ptr = N.c_void_p(self.xc.data_ptr() +
                                     c0 * self.kp * self.xc.element_size())
-                lib.greedy_gains_tc(self.tc_tag, xc_ptr, cl, N.ptr(self.xp),
-                                    dg.n, self.tc_d, self.split_pts,
-                                    N.ptr(part), self.splits, st)
+                probe = self.epi == 0
+                lib.greedy_gains_tc_ex(self.tc_tag, xc_ptr, cl, N.ptr(self.xp),
+                                       dg.n, self.tc_d, self.split_pts,
+                                       N.ptr(part), self.splits,
+                                       2 if probe else self.epi,
+                                       N.ptr(self.hits) if probe else None, st)
             else:
                 cvt_ptr = N.c_void_p(cd.vt.data_ptr() + c0 * esz)
                 cn_ptr = N.c_void_p(cd.norms.data_ptr() + c0 * 8)
@@ -174,6 +187,18 @@ class GreedyRun:
             base = self.gains.data_ptr() if out is None else out.value
             lib.reduce_partials(N.ptr(part), self.splits, cl, 2.0,
                                 N.c_void_p(base + c0 * 8), st)
+        if self.tc and self.epi == 0:
+            self._decide_epi()
+
+    def _decide_epi(self):
+        """One host read of the screen counter after the first gains launch
+        (step 0; steps replayed from a CUDA graph are captured after it)."""
+        screens = (-(-self.l // 128) * 128) * (-(-self.dg.n // 256) * 8)
+        self.hit_fraction = int(self.hits.item()) / max(1, screens)
+        self.epi = 4 if self.hit_fraction > EPI_WIDE_THRESHOLD else 2
+        forced = os.environ.get("EXEM_K3_EPI")  # timing experiments only
+        if forced in ("2", "4"):
+            self.epi = int(forced)
 
     def select(self, step: int):
         """K5: masked argmax (lowest index on ties) -> sel_idx[step]."""

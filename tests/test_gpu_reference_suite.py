@@ -55,6 +55,16 @@ EXPECTED_DEVIATIONS = {
         "parity bound 1e-12 (test_objective.py:40-53)",
 }
 
+# Hypothesis property tests of the reference that can fail on the
+# reference itself (allowed to pass or fail here)
+MAY_FAIL = {
+    "test_core.TestCoalescingLayouts::test_packed_never_worse":
+        "hypothesis finds l=9, k_max=1, d=2, bpv=2, w=8, dim=1, where the "
+        "reference's own count_transactions (core.py:380-403, restated "
+        "unchanged here) gives packed 2 > per-set 1 segments; host-only "
+        "arithmetic, reproduced with PYTHONPATH=/root/reference/pkg/src",
+}
+
 
 def _run_suite(tmp_path):
     xml = tmp_path / "suite.xml"
@@ -97,7 +107,9 @@ def test_reference_suite_against_device(tmp_path):
             fh.write(f"SKIPPED {t}\n")
         fh.write(proc.stdout[-20000:])
     assert passed, proc.stdout[-3000:] + proc.stderr[-3000:]
-    unexpected = [t for t in failed if not any(t.endswith(k) for k in EXPECTED_DEVIATIONS)]
+    unexpected = [t for t in failed
+                  if not any(t.endswith(k) for k in EXPECTED_DEVIATIONS)
+                  and not any(t.endswith(k) for k in MAY_FAIL)]
     stale = [k for k in EXPECTED_DEVIATIONS
              if not any(t.endswith(k) for t in failed)]
     assert not unexpected, "\n".join(f"{t}: {messages.get(t, '')}" for t in unexpected)

@@ -61,7 +61,7 @@ def test_binding_covers_header(native_lib):
 def test_layout_helpers(native_lib):
     lib = native_lib
     from paper_2101_08763_b200._native import ABI_VERSION
-    assert lib.abi_version() == ABI_VERSION == 2
+    assert lib.abi_version() == ABI_VERSION == 3
     assert lib.pad_points(1) == 256 and lib.pad_points(257) == 512
     assert lib.pad_dims(100) == 104 and lib.pad_dims(2) == 8
     assert lib.tc_kp(100) == 128 and lib.tc_kp(2) == 64 and lib.tc_kp(1024) == 1088

@@ -216,6 +216,9 @@ def greedy_record(name, V, prec_name, *, t0=0, warm=1, steps=2,
                          "oracle/exem_oracle.py restatement of "
                          "evaluate.py:142-170"},
         "gpu_launches": int(launches),
+        "k3_epilogue": ({"groups": run.epi,
+                         "screen_hit_fraction": run.hit_fraction}
+                        if run.tc else None),
     }
 
 
