@@ -27,6 +27,8 @@
 //
 // Algorithmic bytes per launch: n*d*4 (V, read once per
 // element group) + 8n (norms) + 4n (aux) + the elements; FFMA work 2*n*k*d.
+#include <cstdlib>
+
 #include "exem_tc_common.cuh"
 
 namespace exem {
@@ -35,7 +37,12 @@ namespace {
 
 constexpr int kP = 256;        // points per tile (= 256 threads)
 constexpr int kThreads = 256;
-constexpr int kStages = 8;     // 8 KB stages: 64 KB in flight per CTA
+#ifndef EXEM_K2_UNROLL_WIDE  // experiment: kk unroll of the wide (EG >= 4) shapes
+#define EXEM_K2_UNROLL_WIDE 8
+#endif
+constexpr int kUnrollWide = EXEM_K2_UNROLL_WIDE;
+constexpr int kMaxStages = 16; // ring depth: as many 8 KB stages as fit
+                               // beside the elements at 2 CTAs per SM
 constexpr int kStageBytes = 8 * 1024;
 constexpr int kElemSmemMax = 128 * 1024;  // resident element budget
 constexpr int kSmemPerSm = 227 * 1024;
@@ -54,16 +61,35 @@ template <> struct Vec4<double> {
 
 constexpr int kWarps = kThreads / 32;
 
-__device__ __forceinline__ bool mbar_test(uint64_t *b, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(ok)
-      : "r"(tc::su32(b)), "r"(parity)
-      : "memory");
-  return ok != 0;
+// mbarrier wait that suspends the warp in hardware until the phase completes
+// (or the time hint elapses) instead of spinning: the spin loop's
+// SYNCS/BRA/ISETP/YIELD were ~15 % of the kernel's issued instructions
+__device__ __forceinline__ void mbar_wait_hint(uint64_t *b, uint32_t parity) {
+  const uint32_t a = tc::su32(b);
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity), "r"(0x989680u)
+        : "memory");
+  } while (!ok);
+}
+
+// (C) x, computed no earlier than `dep` is available: keeps the compiler
+// from converting a prefetched norm right after its load (which would stall
+// the warp on the load at the top of the tile instead of in the epilogue)
+template <typename C> __device__ __forceinline__ C late_cast(double x, C dep);
+template <> __device__ __forceinline__ float late_cast(double x, float dep) {
+  float r;
+  asm volatile("{\n\t.reg .f32 t;\n\tmov.f32 t, %2;\n\tcvt.rn.f32.f64 %0, %1;\n\t}"
+               : "=f"(r) : "d"(x), "f"(dep));
+  return r;
+}
+template <> __device__ __forceinline__ double late_cast(double x, double) {
+  return x;
 }
 
 // partials[tile] = xor tree over the kWarps warp sums of tile iteration tt
@@ -91,10 +117,16 @@ __device__ __forceinline__ void combine_tile(double (&wsum)[2][kWarps],
 // owns ET <= 8 consecutive elements (e = g0 + eg*ET + j), so a group covers
 // KG = EG*ET elements with no dead element columns for any k (k = 10:
 // EG = 2, ET = 5).  Elements live in smem as [dim][EG][8] (8-wide rows).
+// CTAs per SM: each CTA's ring is one serial refill chain, so the
+// HBM-bound shapes (few elements per lane) want more of them (k = 1 at 2
+// CTAs/SM: 0.107 ms, at 4: 0.084 ms); the register budget follows.
+template <int EG>
+constexpr int min_ctas() { return EG == 1 ? 4 : (EG == 2 ? 3 : 2); }
+
 template <int DT, int EG, int ET>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, min_ctas<EG>())
     set_min_tma_kernel(const __grid_constant__ CUtensorMap vmap,
-                       int64_t n, int d_pad,
+                       int64_t n, int d_pad, int nstages,
                        const double *__restrict__ norms,
                        const typename Traits<DT>::C *__restrict__ aux,
                        const typename Traits<DT>::C *__restrict__ elems,
@@ -111,12 +143,14 @@ __global__ void __launch_bounds__(kThreads, 2)
   constexpr int KG = EG * ET;         // elements per group
   constexpr int ROW = EG * 8;         // smem values per dimension
   constexpr int STAGE = BK * kP;      // values per V stage
+  constexpr int kUnrollKK = EG >= 4 ? kUnrollWide : BK;
   // HBM-bound shapes: fetch norms / aux of the tile before its chunk loop
   constexpr bool kPrefetch = PT <= 4;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   C *sv = reinterpret_cast<C *>(smem_raw);          // [S][BK][kP]
-  C *se = sv + kStages * STAGE;                     // [d_pad][EG][8]
-  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
+  C *se = sv + nstages * STAGE;                     // [d_pad][EG][8]
+  __shared__ __align__(8) uint64_t full[kMaxStages];
+  __shared__ uint32_t rel[kMaxStages];  // warps done with a stage's use
   __shared__ __align__(8) uint64_t wfull[2], wempty[2];
   __shared__ double wsum[2][kWarps];
   __shared__ double s_en[KG];
@@ -130,9 +164,9 @@ __global__ void __launch_bounds__(kThreads, 2)
   const int nchunks = d_pad / BK;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < nstages; ++s) {
       tc::mbar_init(&full[s], 1);
-      tc::mbar_init(&empty[s], kWarps);
+      rel[s] = 0;
     }
     for (int s = 0; s < 2; ++s) {
       tc::mbar_init(&wfull[s], kWarps);
@@ -142,30 +176,24 @@ __global__ void __launch_bounds__(kThreads, 2)
   }
   __syncthreads();
 
-  uint32_t ev_issue = 0, ev_use = 0;  // events: (group, tile, chunk)
+  uint32_t ev_use = 0;  // events: (group, tile, chunk)
   const int64_t groups = (k + KG - 1) / KG;
   const uint32_t total = (uint32_t)(groups * my_tiles * nchunks);
-  // Producer (thread 0): event ev's box goes to stage ev % S once the warps
-  // released that stage's previous use.  Blocking only for the event thread
-  // 0 itself needs next; otherwise it tops the ring up with non-blocking
-  // probes, so the producing warp never stalls on the slowest consumer.
-  auto stage_free = [&](uint32_t ev, bool block) -> bool {
-    if (ev < (uint32_t)kStages) return true;
-    const uint32_t par = ((ev / kStages) - 1) & 1;
-    if (block) {
-      tc::mbar_wait(&empty[ev % kStages], par);
-      return true;
-    }
-    return mbar_test(&empty[ev % kStages], par);
-  };
+  // Self-refilling ring: event ev's box goes to stage ev % S.  There is no
+  // producer role: the LAST warp to finish with a stage (a shared-memory
+  // counter) issues that stage's next event, so a refill is never late
+  // behind a busy producing warp.
   auto issue = [&](uint32_t ev) {
-    const int s = ev % kStages;
+    const int s = ev % nstages;
     const uint32_t within = ev % (uint32_t)(my_tiles * nchunks);
     const int64_t tile = blockIdx.x + (int64_t)(within / nchunks) * gridDim.x;
     const int c = (int)(within % nchunks);
     tc::mbar_expect_tx(&full[s], (uint32_t)(STAGE * sizeof(C)));
     tc::tma_load_2d(sv + s * STAGE, &vmap, &full[s], (int)(tile * kP), c * BK);
   };
+  if (threadIdx.x == 0)
+    for (uint32_t ev = 0; ev < total && ev < (uint32_t)nstages; ++ev)
+      issue(ev);
 
   for (int64_t g = 0; g < groups; ++g) {
     const int g0 = (int)(g * KG);
@@ -200,20 +228,11 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
         for (int j = 0; j < ET; ++j) acc[p][j] = C(0);
       for (int c = 0; c < nchunks; ++c, ++ev_use) {
-        if (threadIdx.x == 0) {
-          while (ev_issue <= ev_use) {
-            stage_free(ev_issue, true);
-            issue(ev_issue++);
-          }
-          while (ev_issue < total && ev_issue < ev_use + kStages &&
-                 stage_free(ev_issue, false))
-            issue(ev_issue++);
-        }
-        const int s = ev_use % kStages;
-        tc::mbar_wait(&full[s], (ev_use / kStages) & 1);
+        const int s = ev_use % nstages;
+        mbar_wait_hint(&full[s], (ev_use / nstages) & 1);
         const C *cv = sv + s * STAGE + pg * PT;
         const C *ce = se + (c * BK) * ROW + eg * 8;
-#pragma unroll
+#pragma unroll(kUnrollKK)
         for (int kk = 0; kk < BK; ++kk) {
           C pv[PT], ev[8];
           using V4 = typename Vec4<C>::T;
@@ -251,8 +270,20 @@ __global__ void __launch_bounds__(kThreads, 2)
               }
             }
         }
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&empty[s]);
+        __syncwarp();  // every lane's reads of the stage are consumed
+        if (lane == 0) {
+#ifndef EXEM_K2_NOFENCE
+          __threadfence_block();
+#endif
+          if (atomicAdd(&rel[s], 1u) == (uint32_t)kWarps - 1) {
+            rel[s] = 0;  // no other warp touches it before the refill lands
+            const uint32_t nev = ev_use + (uint32_t)nstages;
+            if (nev < total) {
+              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+              issue(nev);
+            }
+          }
+        }
       }
       // epilogue: distances, first minimum per point within the thread
       // (ascending element index), then across the EG lanes of the point
@@ -266,7 +297,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           nrm[p] = i < n ? norms[i] : 0.0;
           ax[p] = (i < n && include_aux) ? aux[i] : C(0);
         }
-        const C ai = (C)nrm[p];
+        const C ai = late_cast<C>(nrm[p], acc[p][0]);
         C best = tinf<C>();
         int lb = 0;
 #pragma unroll
@@ -350,17 +381,39 @@ cudaError_t launch_t(const CUtensorMap &map, int64_t tiles, int sms,
                      void *t_out, int64_t *label_out, double *partials,
                      void *dist_out, int64_t ldd) {
   using C = typename Traits<DT>::C;
-  const size_t smem = (size_t)kStages * kStageBytes +
-                      (size_t)d_pad * EG * 8 * sizeof(C);
+  const size_t elem_bytes = (size_t)d_pad * EG * 8 * sizeof(C);
+  // 8 KB stages: 5 / 6 / 8 per CTA at 4 / 3 / 2 CTAs per SM (about
+  // 130-170 KB in flight per SM); deeper rings with fewer CTAs measured
+  // slower (13 stages at 2 CTAs: 0.150 vs 0.084 ms at k = 1)
+  int nst = EG == 1 ? 5 : (EG == 2 ? 6 : 8);
+  size_t smem = (size_t)nst * kStageBytes + elem_bytes;
+  while (smem + 4096 > (size_t)kSmemPerSm && nst > 2) {
+    --nst;
+    smem -= kStageBytes;
+  }
+  if (const char *ev = getenv("EXEM_K2_STAGES")) {  // timing experiments only
+    const int want = atoi(ev);
+    if (want >= 2 && want <= kMaxStages &&
+        (size_t)want * kStageBytes + elem_bytes + 4096 <= (size_t)kSmemPerSm) {
+      nst = want;
+      smem = (size_t)nst * kStageBytes + elem_bytes;
+    }
+  }
   cudaError_t e = cudaFuncSetAttribute(
       set_min_tma_kernel<DT, EG, ET>,
       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const int per_sm = smem + 4096 <= kSmemPerSm / 2 ? 2 : 1;
+  int per_sm = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+          &per_sm, set_min_tma_kernel<DT, EG, ET>, kThreads, smem) !=
+          cudaSuccess || per_sm < 1)
+    per_sm = 1;
+  if (const char *ev = getenv("EXEM_K2_MAXCTA"))  // timing experiments only
+    if (atoi(ev) >= 1 && atoi(ev) < per_sm) per_sm = atoi(ev);
   const int grid = (int)(tiles < (int64_t)per_sm * sms ? tiles
                                                        : (int64_t)per_sm * sms);
   set_min_tma_kernel<DT, EG, ET><<<grid, kThreads, smem, st>>>(
-      map, n, d_pad, norms, (const C *)aux, (const C *)elems, enorms, k,
+      map, n, d_pad, nst, norms, (const C *)aux, (const C *)elems, enorms, k,
       include_aux, (C *)t_out, label_out, partials, (C *)dist_out, ldd);
   return cudaGetLastError();
 }
@@ -418,7 +471,8 @@ int set_min_tma(int dtype, const void *vt, int64_t ld, int64_t n, int d_pad,
                        : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                    2, const_cast<void *>(vt), gdim, gstride, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   getenv("EXEM_K2_L2P0") ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                                          : CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return 1;
   const int64_t tiles = ceil_div(n, kP);

@@ -65,6 +65,62 @@ __global__ void __launch_bounds__(256) relu_sum_loop(float *out, int iters,
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// Register outer-product FFMA (the SIMT kernels' inner loop): per thread
+// 8 x 8 accumulators fed by 8 + 8 per-thread register operands, no uniform
+// or immediate operands (FFMA with three general registers).
+__global__ void __launch_bounds__(256) outer_loop(float *out, const float *in,
+                                                  int iters) {
+  float a[8], b[8], acc[8][8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    a[j] = in[(threadIdx.x + j) & 255];
+    b[j] = in[(threadIdx.x + 8 + j) & 255];
+  }
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[r][c] = 0.f;
+#pragma unroll 1
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[r][c] = fmaf(a[r], b[c], acc[r][c]);
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) s += acc[r][c];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+static double run_outer(int sms, int iters) {
+  const int blocks = sms * 2, threads = 256;
+  float *out, *in;
+  cudaMalloc(&out, sizeof(float) * blocks * threads);
+  cudaMalloc(&in, sizeof(float) * 256);
+  cudaMemset(in, 0, sizeof(float) * 256);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  outer_loop<<<blocks, threads>>>(out, in, iters / 10);
+  cudaDeviceSynchronize();
+  float best = 1e30f;
+  for (int r = 0; r < 10; ++r) {
+    cudaEventRecord(e0);
+    outer_loop<<<blocks, threads>>>(out, in, iters);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (ms < best) best = ms;
+  }
+  cudaFree(out);
+  cudaFree(in);
+  return 2.0 * blocks * threads * (double)iters * 64 / (best * 1e-3) / 1e12;
+}
+
 static double run_relu(int sms, int iters, double *ghz) {
   const int blocks = sms * 4, threads = 256;
   float *out;
@@ -138,12 +194,14 @@ int main() {
   const double f32 = run<float>(sms, 20000, &g32);
   const double f64 = run<double>(sms, 4000, &g64);
   const double relu = run_relu(sms, 20000, &gr);
+  const double outer = run_outer(sms, 20000);
   (void)g64;
   printf("{\"sm_count\": %d, \"fp32_ffma_tflops\": %.2f,"
+         " \"fp32_ffma_reg_outer_tflops\": %.2f,"
          " \"fp64_dfma_tflops\": %.2f, \"relu_sum_gpairs\": %.1f,"
          " \"clock_ghz_ffma\": %.3f, \"clock_ghz_relu\": %.3f,"
          " \"how\": \"8 independent FMA chains/thread, %d SMs x 4 CTAs x 256 thr,"
          " best of 10, CUDA events; relu_sum = FMNMX + FADD per pair\"}\n",
-         sms, f32, f64, relu, g32, gr, sms);
+         sms, f32, outer, f64, relu, g32, gr, sms);
   return 0;
 }
