@@ -47,10 +47,17 @@ constexpr int BM = 128;                 // points per tile (TMEM lanes)
 constexpr int A_CHUNK = BM * 128;       // bytes of one point K-chunk
 constexpr int kThreads = 320;
 constexpr int kEpiWarps = 8;
-constexpr int kMaxSpt = 16;             // sets per set tile (register budget of the epilogue)
+// Sets per set tile: up to 16 in the main kernel; small sets (k_max <= 10)
+// use a separate instantiation with up to 32 (N = 16 k_max < 256 left the
+// MMAs short of the sync skeleton; a run-time switch inside one kernel
+// slowed the C5 shape by 17 %, so the wide variant is its own kernel)
+constexpr int kMaxSpt = 16;
+constexpr int kMaxSptWide = 32;
 constexpr int kSmemBudget = 227 * 1024;
-constexpr int kXchBytes = 2 * kMaxSpt * BM * 4;  // epilogue max exchange
-constexpr int kBarBytes = 3072 + kXchBytes;  // barriers, reductions, plain b, exchange
+// barriers, reductions, plain b, and the [2][MAXS][BM] maxima exchange
+__host__ __device__ constexpr int bar_bytes(int maxs) {
+  return 3072 + 2 * maxs * BM * 4;
+}
 constexpr int kTrace = 256;  // tiles traced on CTA 0
 // CTA-0 timeline for timing experiments (tools/tcb_trace.py): compiled in
 // only with -DEXEM_TCB_TRACE_BUILD (EXEM_NVCC_FLAGS at build time) -- the
@@ -146,7 +153,7 @@ struct EpiShape {
   static constexpr int GB = 8;               // 8-column groups per ld batch
 };
 
-// xch: this buffer's [kMaxSpt][BM] exchange slots (set-major, row-minor:
+// xch: this buffer's [MAXS][BM] exchange slots (set-major, row-minor:
 // conflict-free).
 template <int SPT, int HH, bool kPlain, typename Release>
 __device__ __forceinline__ void epi_tile(
@@ -204,7 +211,7 @@ __device__ __forceinline__ void epi_tile(
 // The epilogue warps' whole loop for one sets-per-tile count (SPT at compile
 // time, so every column's set and the accumulator array are static) and one
 // group parity HH.  Work items follow the producer's order (item_of).
-template <int SPT, int HH, bool kPlain>
+template <int SPT, int HH, bool kPlain, int MAXS>
 __device__ __forceinline__ void epilogue_role(const BParams &p, uint32_t tmem,
                                               uint64_t *tfull,
                                               uint64_t *tempty, double *red,
@@ -268,10 +275,10 @@ __device__ __forceinline__ void epilogue_role(const BParams &p, uint32_t tmem,
           }
         } trel{rel, p, tr, etile};
         epi_tile<SPT, HH, kPlain>(taddr, ngroups, q, row, ax, ha, valid, bsm,
-                                  xch + buf * (kMaxSpt * BM), acc, trel);
+                                  xch + buf * (MAXS * BM), acc, trel);
 #else
         epi_tile<SPT, HH, kPlain>(taddr, ngroups, q, row, ax, ha, valid, bsm,
-                                  xch + buf * (kMaxSpt * BM), acc, rel);
+                                  xch + buf * (MAXS * BM), acc, rel);
 #endif
       }
 #ifdef EXEM_TCB_TRACE_BUILD
@@ -289,7 +296,7 @@ __device__ __forceinline__ void epilogue_role(const BParams &p, uint32_t tmem,
         double v = acc[k];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0) red[q * kMaxSpt + s] = v;
+        if (lane == 0) red[q * MAXS + s] = v;
       }
     }
     asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
@@ -297,8 +304,8 @@ __device__ __forceinline__ void epilogue_role(const BParams &p, uint32_t tmem,
       const int64_t j = st * SPT + lane;  // >= l for a cluster's spare tile
       if (lane < SPT && j < p.l)
         p.partial[sp * p.l + j] =
-            ((red[lane] + red[kMaxSpt + lane]) + red[2 * kMaxSpt + lane]) +
-            red[3 * kMaxSpt + lane];
+            ((red[lane] + red[MAXS + lane]) + red[2 * MAXS + lane]) +
+            red[3 * MAXS + lane];
     }
     asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
   }
@@ -397,7 +404,7 @@ __device__ __forceinline__ void release_stage(uint64_t *bar) {
 
 // MC: CTAs per cluster sharing every point tile by TMA multicast (1 = none).
 // map_p: the point operand with BM/MC-row boxes.
-template <int MC>
+template <int MC, int MAXS>
 __global__ void __launch_bounds__(kThreads, 1)
     batch_tc_kernel(const __grid_constant__ CUtensorMap map_p,
                     const __grid_constant__ CUtensorMap map_s,
@@ -419,9 +426,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t *bfull = tempty + 2;                    // [1]
   uint64_t *bempty = bfull + 1;                    // [1]
   uint32_t *tmem_slot = (uint32_t *)(bempty + 1);
-  double *red = (double *)(tmem_slot + 4);         // [4][kMaxSpt]
-  float *bsm = (float *)(red + 4 * kMaxSpt);       // [256] plain: set b
-  float *xch = bsm + 256;                          // [2][kMaxSpt][BM]
+  double *red = (double *)(tmem_slot + 4);         // [4][MAXS]
+  float *bsm = (float *)(red + 4 * MAXS);          // [256] plain: set b
+  float *xch = bsm + 256;                          // [2][MAXS][BM]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   WorkSplit ws;
@@ -654,9 +661,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     // -------------------------------------------------------------- epilogue
     const bool hh = (warp - 2) >= 4;  // 8-column group parity of this warp
-    switch (p.spt) {
-#define EXEM_EPI_ROLE(S, H, PL) \
-  epilogue_role<S, H, PL>(p, tmem, tfull, tempty, red, bsm, xch, warp, lane, ws)
+#define EXEM_EPI_ROLE(S, H, PL)                                              \
+  epilogue_role<S, H, PL, MAXS>(p, tmem, tfull, tempty, red, bsm, xch, warp, \
+                                lane, ws)
 #define EXEM_EPI_CASE(S)                                                     \
   case S:                                                                    \
     if (p.plain) {                                                           \
@@ -665,14 +672,26 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (hh) EXEM_EPI_ROLE(S, 1, false); else EXEM_EPI_ROLE(S, 0, false);   \
     }                                                                        \
     break;
-      EXEM_EPI_CASE(1) EXEM_EPI_CASE(2) EXEM_EPI_CASE(3) EXEM_EPI_CASE(4)
-      EXEM_EPI_CASE(5) EXEM_EPI_CASE(6) EXEM_EPI_CASE(7) EXEM_EPI_CASE(8)
-      EXEM_EPI_CASE(9) EXEM_EPI_CASE(10) EXEM_EPI_CASE(11) EXEM_EPI_CASE(12)
-      EXEM_EPI_CASE(13) EXEM_EPI_CASE(14) EXEM_EPI_CASE(15) EXEM_EPI_CASE(16)
+    // each instantiation compiles only its own set-count class
+    if constexpr (MAXS == kMaxSpt) {
+      switch (p.spt) {
+        EXEM_EPI_CASE(1) EXEM_EPI_CASE(2) EXEM_EPI_CASE(3) EXEM_EPI_CASE(4)
+        EXEM_EPI_CASE(5) EXEM_EPI_CASE(6) EXEM_EPI_CASE(7) EXEM_EPI_CASE(8)
+        EXEM_EPI_CASE(9) EXEM_EPI_CASE(10) EXEM_EPI_CASE(11) EXEM_EPI_CASE(12)
+        EXEM_EPI_CASE(13) EXEM_EPI_CASE(14) EXEM_EPI_CASE(15) EXEM_EPI_CASE(16)
+        default: break;
+      }
+    } else {
+      switch (p.spt) {
+        EXEM_EPI_CASE(17) EXEM_EPI_CASE(18) EXEM_EPI_CASE(19) EXEM_EPI_CASE(20)
+        EXEM_EPI_CASE(21) EXEM_EPI_CASE(22) EXEM_EPI_CASE(23) EXEM_EPI_CASE(24)
+        EXEM_EPI_CASE(25) EXEM_EPI_CASE(26) EXEM_EPI_CASE(27) EXEM_EPI_CASE(28)
+        EXEM_EPI_CASE(29) EXEM_EPI_CASE(30) EXEM_EPI_CASE(31) EXEM_EPI_CASE(32)
+        default: break;
+      }
+    }
 #undef EXEM_EPI_CASE
 #undef EXEM_EPI_ROLE
-      default: break;
-    }
   }
 
   fence_before();
@@ -754,12 +773,12 @@ __global__ void pack_plain_kernel(const float *__restrict__ vt, int64_t ld,
 }
 
 // Launch one persistent CTA per SM (clusters of MC), at most one per unit.
-template <int MC>
+template <int MC, int MAXS>
 cudaError_t launch_batch(const BParams &prm, const CUtensorMap &mp,
                          const CUtensorMap &ms, size_t smem, int sms,
                          int64_t splits, void *stream) {
   cudaError_t e = cudaFuncSetAttribute(
-      batch_tc_kernel<MC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      batch_tc_kernel<MC, MAXS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
       (int)smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
@@ -778,7 +797,8 @@ cudaError_t launch_batch(const BParams &prm, const CUtensorMap &mp,
     cfg.numAttrs = 1;
     cfg.gridDim = dim3((unsigned)(clusters * MC));
     int active = 0;
-    e = cudaOccupancyMaxActiveClusters(&active, batch_tc_kernel<MC>, &cfg);
+    e = cudaOccupancyMaxActiveClusters(&active, batch_tc_kernel<MC, MAXS>,
+                                       &cfg);
     if (e != cudaSuccess) return e;
     if (active < 1) return cudaErrorLaunchOutOfResources;
     if (active < clusters) clusters = active;
@@ -786,10 +806,10 @@ cudaError_t launch_batch(const BParams &prm, const CUtensorMap &mp,
   if (units < clusters) clusters = units;
   cfg.gridDim = dim3((unsigned)(clusters * MC));
   if (getenv("EXEM_TCB_VERBOSE"))
-    fprintf(stderr, "batch_tc<%d>: grid=%u stages=%d smem=%zu bstream=%d "
-            "tstage=%d gch=%d\n", MC, cfg.gridDim.x, prm.stages, smem,
+    fprintf(stderr, "batch_tc<%d,%d>: grid=%u stages=%d smem=%zu bstream=%d "
+            "tstage=%d gch=%d\n", MC, MAXS, cfg.gridDim.x, prm.stages, smem,
             prm.bstream, prm.tstage, prm.gch);
-  return cudaLaunchKernelEx(&cfg, batch_tc_kernel<MC>, mp, ms, prm);
+  return cudaLaunchKernelEx(&cfg, batch_tc_kernel<MC, MAXS>, mp, ms, prm);
 }
 
 }  // namespace tcb
@@ -808,7 +828,11 @@ int exem_tc_set_geometry(int64_t k_max, int32_t *spt, int32_t *w,
                 "tcgen05 batch path holds a set in <= 256 TMEM columns "
                 "(k_max=%lld)", (long long)k_max);
   int64_t s = 256 / ww;
-  if (s > tcb::kMaxSpt) s = tcb::kMaxSpt;
+  // more than 16 sets per tile (the small-set kernel) only where it wins:
+  // k_max <= 10 (d = 100 / 256: k = 5 +14 % / +65 %, k = 8 +9 % / +40 %,
+  // k = 10 +3 % / +12 %; k = 12..15 0 to -14 %, profiles/r02_k4_small_sets.log)
+  if (s > tcb::kMaxSpt && ww > 10) s = tcb::kMaxSpt;
+  if (s > tcb::kMaxSptWide) s = tcb::kMaxSptWide;
   if (const char *e = getenv("EXEM_TCB_SPT")) {  // timing experiments only
     const int64_t f = atoll(e);
     if (f >= 1 && f < s) s = f;
@@ -940,6 +964,8 @@ int exem_batch_eval_tc(int dtype, const void *xp, int64_t n, const void *aux,
     cudaMemset(prm.trace, 0, 16 * kTrace * sizeof(long long));
   }
   const int b_chunk = nc * 128;
+  const int maxs = spt > kMaxSpt ? kMaxSptWide : kMaxSpt;
+  const int kBarBytes = bar_bytes(maxs);
   const int avail = kSmemBudget - kBarBytes - 1024;
   // set tile stationary when it leaves room for >= 3 point-chunk stages
   const bool bstream = (avail - prm.kchunks * b_chunk) / A_CHUNK < 3;
@@ -981,10 +1007,17 @@ int exem_batch_eval_tc(int dtype, const void *xp, int64_t n, const void *aux,
   if (int rc = make_map(&ms, xs, dtype, exem_tc_set_rows(l, k_max), kp, nc))
     return rc;
   cudaError_t e;
-  switch (mc) {
-    case 1: e = launch_batch<1>(prm, mp, ms, smem, sms, splits, stream); break;
-    case 4: e = launch_batch<4>(prm, mp, ms, smem, sms, splits, stream); break;
-    default: e = launch_batch<2>(prm, mp, ms, smem, sms, splits, stream); break;
+  if (maxs == kMaxSptWide) {  // small sets: the 32-set-tile kernel
+    e = mc == 1 ? launch_batch<1, kMaxSptWide>(prm, mp, ms, smem, sms, splits,
+                                               stream)
+                : launch_batch<2, kMaxSptWide>(prm, mp, ms, smem, sms, splits,
+                                               stream);
+  } else {
+    switch (mc) {
+      case 1: e = launch_batch<1, kMaxSpt>(prm, mp, ms, smem, sms, splits, stream); break;
+      case 4: e = launch_batch<4, kMaxSpt>(prm, mp, ms, smem, sms, splits, stream); break;
+      default: e = launch_batch<2, kMaxSpt>(prm, mp, ms, smem, sms, splits, stream); break;
+    }
   }
   if (e != cudaSuccess)
     return fail(EXEM_ERR_CUDA, "batch_tc_kernel launch: %s",

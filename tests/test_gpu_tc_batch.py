@@ -9,7 +9,8 @@ tests/contract.py):
 
 and the reference's own half bound (5e-2 vs binary32) through
 test_gpu_parity.py.  Geometry cases cover: one set per tile (k_max = 256),
-many sets per tile (k_max = 1 -> 16 sets of 8 columns), ragged
+many sets per tile (k_max = 1 -> 32 sets; k_max <= 10 runs the 17-32
+set-per-tile kernel), ragged
 cardinalities (blank slots), l not a multiple of the sets per tile, n not a
 multiple of the 128-point tile with several partial-sum splits, the
 stationary set tile with whole / per-chunk point stages (d <= 256) and the
@@ -51,8 +52,12 @@ def _check(g, sets, vals, nref=None, label="K4-TC"):
 @pytest.mark.parametrize("prec", [BF16, P16])
 @pytest.mark.parametrize("n,d,l,kmin,kmax", [
     (3000, 100, 150, 1, 50),      # ragged, 5 interleaved sets in N = 256
-    (1000, 2, 70, 1, 1),          # k_max = 1: 16 sets in N = 16
-    (2500, 16, 45, 8, 8),         # 16 sets of 8 in N = 128
+    (1000, 2, 70, 1, 1),          # k_max = 1: 32 sets in N = 32
+    (2500, 16, 45, 8, 8),         # 32 sets of 8 in N = 256 (wide kernel)
+    (4000, 100, 120, 10, 10),     # 25 sets of 10 in N = 256 (wide kernel)
+    (3000, 64, 61, 2, 9),         # 28 sets of 9 (wide kernel, ragged)
+    (3000, 64, 61, 2, 15),        # 16 sets of 15 (main kernel, ragged)
+    (2000, 100, 40, 1, 16),       # 16 sets of 16: the main kernel
     (1300, 256, 20, 1, 256),      # one set per tile, per-chunk point stages
     (777, 700, 9, 3, 40),         # streamed set tile (d > stationary budget)
     (20_000, 37, 33, 1, 12),      # several splits, n % 128 != 0

@@ -286,7 +286,9 @@ def test_stream_plan_is_split_aligned(native_lib):
 
 def test_tc_set_geometry(native_lib):
     """K4-TC set tiles: w = k_max slots per set (column-interleaved), as many
-    sets as fit 256 TMEM columns (<= 16), MMA N = round_up(spt*w, 16)."""
+    sets as fit 256 TMEM columns (<= 16; <= 32 in the small-set kernel,
+    k_max <= 10),
+    MMA N = round_up(spt*w, 16)."""
     import ctypes
 
     geo = native_lib.raw("exem_tc_set_geometry")
@@ -294,7 +296,7 @@ def test_tc_set_geometry(native_lib):
         spt, w, nc = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
         assert geo(k, ctypes.byref(spt), ctypes.byref(w), ctypes.byref(nc)) == 0
         assert w.value == k
-        assert spt.value == min(16, 256 // k)
+        assert spt.value == (min(32, 256 // k) if k <= 10 else min(16, 256 // k))
         assert nc.value == -(-spt.value * k // 16) * 16 <= 256
         rows = native_lib.tc_set_rows(1000, k)
         assert rows == -(-1000 // spt.value) * nc.value

@@ -121,6 +121,57 @@ static double run_outer(int sms, int iters) {
   return 2.0 * blocks * threads * (double)iters * 64 / (best * 1e-3) / 1e12;
 }
 
+// The relu-sum as the K3-TC epilogue now computes it: per value pair one
+// FADD2 forming (x + |x|) = 2 max(0, x) for both values and one FADD2 adding
+// them to a pair of running sums (1 instruction per value).  x is another
+// chain's sum, so nothing is hoisted; 8 independent pairs per thread.
+__global__ void __launch_bounds__(256) relu_fadd2_loop(float *out, int iters) {
+  float2 acc[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    acc[j] = make_float2((float)(threadIdx.x + j) - 128.f, (float)j - 3.f);
+#pragma unroll 1
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float2 x = acc[(j + 1) & 7];
+        const float2 ax = make_float2(fabsf(x.x), fabsf(x.y));
+        acc[j] = __fadd2_rn(acc[j], __fadd2_rn(x, ax));
+      }
+    }
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) s += acc[j].x + acc[j].y;
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+static double run_relu2(int sms, int iters) {
+  const int blocks = sms * 4, threads = 256;
+  float *out;
+  cudaMalloc(&out, sizeof(float) * blocks * threads);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  relu_fadd2_loop<<<blocks, threads>>>(out, iters / 10);
+  cudaDeviceSynchronize();
+  float best = 1e30f;
+  for (int r = 0; r < 10; ++r) {
+    cudaEventRecord(e0);
+    relu_fadd2_loop<<<blocks, threads>>>(out, iters);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (ms < best) best = ms;
+  }
+  cudaFree(out);
+  const double vals = (double)blocks * threads * iters * 16 * 8 * 2;
+  return vals / (best * 1e-3) / 1e9;  // G values/s
+}
+
 static double run_relu(int sms, int iters, double *ghz) {
   const int blocks = sms * 4, threads = 256;
   float *out;
@@ -195,13 +246,15 @@ int main() {
   const double f64 = run<double>(sms, 4000, &g64);
   const double relu = run_relu(sms, 20000, &gr);
   const double outer = run_outer(sms, 20000);
+  const double relu2 = run_relu2(sms, 20000);
   (void)g64;
   printf("{\"sm_count\": %d, \"fp32_ffma_tflops\": %.2f,"
          " \"fp32_ffma_reg_outer_tflops\": %.2f,"
          " \"fp64_dfma_tflops\": %.2f, \"relu_sum_gpairs\": %.1f,"
+         " \"relu_sum_fadd2_gpairs\": %.1f,"
          " \"clock_ghz_ffma\": %.3f, \"clock_ghz_relu\": %.3f,"
          " \"how\": \"8 independent FMA chains/thread, %d SMs x 4 CTAs x 256 thr,"
          " best of 10, CUDA events; relu_sum = FMNMX + FADD per pair\"}\n",
-         sms, f32, outer, f64, relu, g32, gr, sms);
+         sms, f32, outer, f64, relu, relu2, g32, gr, sms);
   return 0;
 }
