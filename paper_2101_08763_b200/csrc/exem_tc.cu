@@ -252,11 +252,11 @@ __device__ __forceinline__ void relu_acc_fmnmx(const uint32_t (&r)[32],
 // acc.x += 2 max(0, r[2j]), acc.y += 2 max(0, r[2j+1]) in ascending j.
 // x + |x| is exactly 2 max(0, x) (0 or 2x), and one FADD2 with the |.|
 // operand modifier forms it for a register pair; a second FADD2 adds the
-// pair to the two running sums: 1 instruction per value instead of
-// FMNMX + FADD (the epilogue is issue-bound at 2 instructions per value on
-// data with many positive gains; tools/epi_probe.cu).  The doubled sums are
-// halved once (exact), so they equal the FMNMX + FADD sums bit for bit
-// unless a partial sum is subnormal.
+// pair to the two running sums.  FADD2 issues at half the FADD rate, so this
+// runs at the FMNMX + FADD speed (tools/simt_peak.cu: 18.6 vs 18.3 T
+// values/s) while keeping the ALU pipe free for the sign screens.  The
+// doubled sums are halved once (exact), so they equal the FMNMX + FADD sums
+// bit for bit unless a partial sum is subnormal.
 __device__ __forceinline__ void relu_acc(const uint32_t (&r)[32],
                                          float2 &acc) {
 #pragma unroll
