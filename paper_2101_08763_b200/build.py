@@ -16,7 +16,8 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libexem_b200.so"
-SOURCES = [CSRC / "exem_simt.cu", CSRC / "exem_setmin.cu", CSRC / "exem_tc.cu",
+SOURCES = [CSRC / "exem_simt.cu", CSRC / "exem_setmin.cu",
+           CSRC / "exem_simt_tma.cu", CSRC / "exem_tc.cu",
            CSRC / "exem_tc_batch.cu"]
 HEADERS = [CSRC / "exem_common.cuh", CSRC / "exem_tc_common.cuh",
            ROOT / "include" / "exem_b200.h"]

@@ -213,6 +213,14 @@ __global__ void __launch_bounds__(kRedThreads)
   if (threadIdx.x == 0) partials[blockIdx.x] = r;
 }
 
+// TMA-fed K3-SIMT (exem_simt_tma.cu): 0 launched, 1 not applicable, < 0 a
+// CUDA error
+int gains_simt_tma(int dtype, const void *cvt, int64_t ldc,
+                   const double *cnorms, int64_t l, const void *vt, int64_t ld,
+                   const double *norms, const void *m, int64_t n, int d_pad,
+                   int64_t split_pts, int64_t splits, double *partial,
+                   cudaStream_t st);
+
 // TMA-fed persistent K2 (exem_setmin.cu): 0 launched, 1 shape not covered,
 // < 0 a CUDA error
 int set_min_tma(int dtype, const void *vt, int64_t ld, int64_t n, int d_pad,
@@ -1421,6 +1429,18 @@ int exem_greedy_gains_simt(int dtype, const void *cvt, int64_t ldc,
     return fail(EXEM_ERR_ARG, "greedy_gains_simt: leading dims not padded");
   cudaStream_t st = (cudaStream_t)stream;
   const int d_pad = (int)exem_pad_dims(d);
+  // the TMA-fed kernel (exem_simt_tma.cu) when its tensor maps apply
+  {
+    const int r = gains_simt_tma(dtype, cvt, ldc, cnorms, l, vt, ld, norms, m,
+                                 n, d_pad, split_pts, splits, partial, st);
+    if (r == 0) {
+      count_launch();
+      return EXEM_OK;
+    }
+    if (r < 0)
+      return fail(EXEM_ERR_CUDA, "gains_simt_tma_kernel: %s",
+                  cudaGetErrorString((cudaError_t)(-r)));
+  }
   dim3 grid((unsigned)ceil_div(l, kBM), (unsigned)splits);
   // fp64: k-chunks of 16 (half the ring barriers per DFMA) when d_pad allows
   // it without extra padding -- d = 512 / 1024: 436 -> 413 / 866 -> 822 ms;
