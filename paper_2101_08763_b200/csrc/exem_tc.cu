@@ -257,8 +257,13 @@ __device__ __forceinline__ void relu_acc_fmnmx(const uint32_t (&r)[32],
 // values/s) while keeping the ALU pipe free for the sign screens.  The
 // doubled sums are halved once (exact), so they equal the FMNMX + FADD sums
 // bit for bit unless a partial sum is subnormal.
+// Four independent FADD2 chains per 32 values (pairs j = 4q + c go to chain
+// c), combined in a fixed tree: the chain's latency, not the FADD2 issue
+// rate, bounded a warp's relu-sum when most chunks fire (16 dependent FADD2
+// per chunk behind each taken sign-screen branch).
 __device__ __forceinline__ void relu_acc(const uint32_t (&r)[32],
                                          float2 &acc) {
+#ifdef EXEM_TC_RELU_CHAIN1  // A/B experiment: one chain per 32 values
 #pragma unroll
   for (int j = 0; j < 32; j += 2) {
     const float2 x = make_float2(__uint_as_float(r[j]),
@@ -266,6 +271,24 @@ __device__ __forceinline__ void relu_acc(const uint32_t (&r)[32],
     const float2 ax = make_float2(fabsf(x.x), fabsf(x.y));
     acc = __fadd2_rn(acc, __fadd2_rn(x, ax));
   }
+#else
+  float2 c[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float2 x = make_float2(__uint_as_float(r[2 * q]),
+                                 __uint_as_float(r[2 * q + 1]));
+    c[q] = __fadd2_rn(x, make_float2(fabsf(x.x), fabsf(x.y)));
+  }
+#pragma unroll
+  for (int j = 8; j < 32; j += 2) {
+    const float2 x = make_float2(__uint_as_float(r[j]),
+                                 __uint_as_float(r[j + 1]));
+    const float2 ax = make_float2(fabsf(x.x), fabsf(x.y));
+    c[(j >> 1) & 3] = __fadd2_rn(c[(j >> 1) & 3], __fadd2_rn(x, ax));
+  }
+  acc = __fadd2_rn(acc, __fadd2_rn(__fadd2_rn(c[0], c[1]),
+                                   __fadd2_rn(c[2], c[3])));
+#endif
 }
 
 

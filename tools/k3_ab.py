@@ -16,8 +16,13 @@ CHILD = r'''
 import sys, json
 sys.path.insert(0, %r); sys.path.insert(0, %r)
 import bench_configs as B
-V = B.blobs(1_000_000, 100, 3) if %r == "blobs" else B.gaussian(1_000_000, 100, 0)
-r = B.greedy_record("ab", V, "bf16", warm=3, steps=5, cpu_seconds=0.0)
+kind = %r
+if kind in ("gauss", "blobs"):
+    V = B.blobs(1_000_000, 100, 3) if kind == "blobs" else B.gaussian(1_000_000, 100, 0)
+    r = B.greedy_record("ab", V, "bf16", warm=3, steps=5, cpu_seconds=0.0)
+else:  # c3d<d>: the C3 sweep shape (n = 100k, |S u c| = 50)
+    r = B.greedy_record("ab", B.gaussian(100_000, int(kind[3:]), 0), "bf16",
+                        t0=47, warm=1, steps=2, cpu_seconds=0.0)
 print(json.dumps({"ms": r["ms_per_step"], "kms": r["roofline"]["kernel_ms_avg"],
                   "epi": r["k3_epilogue"]}))
 '''
@@ -28,7 +33,7 @@ def main():
     libs = dict(a.split("=", 1) for a in sys.argv[1:])
     out = {}
     for rep in range(2):
-        for data in ("gauss", "blobs"):
+        for data in os.environ.get("K3AB_DATA", "gauss,blobs").split(","):
             for name, path in libs.items():
                 lib, _, epi = path.partition(":")
                 env = dict(os.environ, EXEM_LIB_PATH=str(Path(lib).resolve()))
