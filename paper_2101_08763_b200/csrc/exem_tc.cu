@@ -191,12 +191,15 @@ __device__ __forceinline__ void mma_item_waits(
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) {
       if (ks == WT && more) {
+        TR(0, s.tile_no + 1);
         mbar_wait(&tempty[nbuf], ((s.tph >> nbuf) & 1u) ^ 1u);
+        TR(1, s.tile_no + 1);
         s.tph ^= 1u << nbuf;
         fence_after();
       }
       if (ks == WF && more) {
         mbar_wait(&full[nstage], nph);
+        TR(2, s.tile_no + 1);
         fence_after();
       }
       constexpr uint32_t kA = 128 * 128 >> 4, kB = 256 * 128 >> 4;
@@ -209,13 +212,17 @@ __device__ __forceinline__ void mma_item_waits(
     else
       umma_commit(&empty[s.stage]);
     umma_commit(&tfull[s.buf]);
+    TR(3, s.tile_no);
     if (WT == KS && more) {
+      TR(0, s.tile_no + 1);
       mbar_wait(&tempty[nbuf], ((s.tph >> nbuf) & 1u) ^ 1u);
+      TR(1, s.tile_no + 1);
       s.tph ^= 1u << nbuf;
       fence_after();
     }
     if (WF == KS && more) {
       mbar_wait(&full[nstage], nph);
+      TR(2, s.tile_no + 1);
       fence_after();
     }
     ++s.tile_no;
