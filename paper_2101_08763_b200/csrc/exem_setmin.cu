@@ -61,23 +61,6 @@ template <> struct Vec4<double> {
 
 constexpr int kWarps = kThreads / 32;
 
-// mbarrier wait that suspends the warp in hardware until the phase completes
-// (or the time hint elapses) instead of spinning: the spin loop's
-// SYNCS/BRA/ISETP/YIELD were ~15 % of the kernel's issued instructions
-__device__ __forceinline__ void mbar_wait_hint(uint64_t *b, uint32_t parity) {
-  const uint32_t a = tc::su32(b);
-  uint32_t ok = 0;
-  do {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(a), "r"(parity), "r"(0x989680u)
-        : "memory");
-  } while (!ok);
-}
-
 // (C) x, computed no earlier than `dep` is available: keeps the compiler
 // from converting a prefetched norm right after its load (which would stall
 // the warp on the load at the top of the tile instead of in the epilogue)
@@ -229,7 +212,9 @@ __global__ void __launch_bounds__(kThreads, min_ctas<EG>())
         for (int j = 0; j < ET; ++j) acc[p][j] = C(0);
       for (int c = 0; c < nchunks; ++c, ++ev_use) {
         const int s = ev_use % nstages;
-        mbar_wait_hint(&full[s], (ev_use / nstages) & 1);
+        // suspend in hardware until the box lands (a spin loop's
+        // SYNCS/BRA/ISETP/YIELD were ~15 % of the issued instructions)
+        tc::mbar_wait_hint(&full[s], (ev_use / nstages) & 1);
         const C *cv = sv + s * STAGE + pg * PT;
         const C *ce = se + (c * BK) * ROW + eg * 8;
 #pragma unroll(kUnrollKK)

@@ -30,20 +30,6 @@ constexpr int kTM = 128, kTN = 128, kThr = 256, kWarps = kThr / 32;
 // ring depth: 4 stages of 16-dimension chunks or 8 of 8 (d_pad % 16 != 0)
 template <int BK> constexpr int stages_of() { return BK == 16 ? 4 : 8; }
 
-__device__ __forceinline__ void wait_full(uint64_t *b, uint32_t parity) {
-  const uint32_t a = tc::su32(b);
-  uint32_t ok = 0;
-  do {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(a), "r"(parity), "r"(0x989680u)
-        : "memory");
-  } while (!ok);
-}
-
 __device__ __forceinline__ int toff(int t4, int r) {
   return r < 4 ? t4 * 4 + r : 64 + t4 * 4 + (r - 4);
 }
@@ -116,7 +102,7 @@ __global__ void __launch_bounds__(kThr, sizeof(T) == 4 ? 2 : 1)
         acc[r][c] = -(s_h[toff(tx, c)] + s_b[toff(ty, r)]);
     for (int c = 0; c < nk; ++c, ++ev) {
       const int s = ev % kStages;
-      wait_full(&full[s], (ev / kStages) & 1);
+      tc::mbar_wait_hint(&full[s], (ev / kStages) & 1);
       const T *sa = ring + s * STAGE;
       const T *sb = sa + BK * kTM;
 #pragma unroll

@@ -615,7 +615,11 @@ __global__ void __launch_bounds__(Epi<kQ>::kThreads, 1)
           if (TC_WAIT_SPIN(p))
             mbar_wait(&tfull[buf], (tph >> buf) & 1u);
           else
+#ifdef EXEM_TC_EPI_SLEEP  // A/B experiment: nanosleep back-off (round 1)
             mbar_wait_sleep(&tfull[buf], (tph >> buf) & 1u);
+#else
+            mbar_wait_hint(&tfull[buf], (tph >> buf) & 1u);
+#endif
         }
         __syncwarp();
         if (tr) TR(5, tile_no);

@@ -65,6 +65,22 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t *b, uint32_t parity) {
     __nanosleep(EXEM_TC_SLEEP_NS);
   }
 }
+// Wait that suspends the thread in hardware until the phase completes (or
+// the time hint elapses): wakes as soon as the barrier flips, without the
+// coarse granularity of a nanosleep back-off or the issue slots of a spin.
+__device__ __forceinline__ void mbar_wait_hint(uint64_t *b, uint32_t parity) {
+  const uint32_t a = su32(b);
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity), "r"(0x989680u)
+        : "memory");
+  } while (!ok);
+}
 __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map,
                                             uint64_t *bar, int x, int y) {
   asm volatile(
