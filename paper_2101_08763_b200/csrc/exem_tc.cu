@@ -43,8 +43,8 @@ constexpr int B_CHUNK = BN * 128;  // bytes of one B K-chunk
 // the tile period and Q = 4 is 16 % faster; on data where the sign screen
 // skips almost everything (centred Gaussian) Q = 2 is 2 % faster
 // (tools/k3_ab.py).
-template <int Q> struct Epi {
-  static constexpr int kCols = BN / Q;        // accumulator columns per warp
+template <int Q, int BNv = BN> struct Epi {
+  static constexpr int kCols = BNv / Q;       // accumulator columns per warp
   static constexpr int kWarps = 4 * Q;        // epilogue warps
   static constexpr int kThreads = 64 + 32 * kWarps;
   // Role warps.  The SMSP arbiter favours the highest warp id, so the
@@ -56,7 +56,7 @@ template <int Q> struct Epi {
   static constexpr int kMmaWarp = kWarps + 1;
 };
 constexpr int kSmemBudget = 227 * 1024;
-constexpr int kBarBytes = 1024;
+constexpr int kBarBytes = 2048;  // barriers (<= 4 TMEM buffers), slot, red
 constexpr int kTrace = 256;  // tiles traced on CTA 0 (EXEM_TC_TRACE)
 // CTA-0 timeline (EXEM_TC_TRACE, tools/tc_trace.py): probe builds only
 // (-DEXEM_TC_PROBE_BUILD), like the EXEM_TC_DEBUG masks.
@@ -126,12 +126,12 @@ __device__ __forceinline__ void umma_chunk_n(int nk, uint32_t d, uint64_t ad,
 // All K steps of one whole-tile stage, fully unrolled (compile-time
 // descriptor offsets): A chunks are A_CHUNK apart, B chunks B_CHUNK apart,
 // K=16 steps 32 B apart inside a 128-B swizzle row.
-template <int KS>
+template <int KS, int BNv = BN>
 __device__ __forceinline__ void issue_tile(uint32_t d, uint64_t a0,
                                            uint64_t b0, uint32_t idesc) {
 #pragma unroll
   for (int ks = 0; ks < KS; ++ks) {
-    constexpr uint32_t kA = 128 * 128 >> 4, kB = 256 * 128 >> 4;
+    constexpr uint32_t kA = 128 * 128 >> 4, kB = BNv * 128 >> 4;
     umma_f16(d, a0 + (uint64_t)((ks >> 2) * kA + (ks & 3) * 2),
              b0 + (uint64_t)((ks >> 2) * kB + (ks & 3) * 2), idesc,
              ks > 0 ? 1u : 0u);
@@ -139,12 +139,12 @@ __device__ __forceinline__ void issue_tile(uint32_t d, uint64_t a0,
 }
 
 // MMAs [LO, HI) of one whole-tile stage.
-template <int LO, int HI>
+template <int LO, int HI, int BNv = BN>
 __device__ __forceinline__ void issue_range(uint32_t d, uint64_t a0,
                                             uint64_t b0, uint32_t idesc) {
 #pragma unroll
   for (int ks = LO; ks < HI; ++ks) {
-    constexpr uint32_t kA = 128 * 128 >> 4, kB = 256 * 128 >> 4;
+    constexpr uint32_t kA = 128 * 128 >> 4, kB = BNv * 128 >> 4;
     umma_f16(d, a0 + (uint64_t)((ks >> 2) * kA + (ks & 3) * 2),
              b0 + (uint64_t)((ks >> 2) * kB + (ks & 3) * 2), idesc,
              ks > 0 ? 1u : 0u);
@@ -168,7 +168,7 @@ struct MmaState {
 // (tools/k3_waits.sh, profiles/r01_k3_waits.log): WF = KS-2, WT = KS-1 is
 // 6 % faster than both before KS-2 (185.4 -> 173.5 ms); waiting for tempty
 // after the tile costs 25 %.
-template <int KS, int WF, int WT, int CS, typename P>
+template <int KS, int WF, int WT, int CS, int BNv, typename P>
 __device__ __forceinline__ void mma_item_waits(
     const P &p, int ntiles, MmaState &s, uint64_t a_desc0, uint64_t b_desc0,
     uint32_t stage_step, uint32_t tmem, uint64_t *full, uint64_t *empty,
@@ -178,9 +178,10 @@ __device__ __forceinline__ void mma_item_waits(
   mbar_wait(&full[s.stage], s.ph);
   fence_after();
   for (int t = 0; t < ntiles; ++t) {
-    const uint32_t d = tmem + s.buf * 256u;
+    constexpr uint32_t kNB = 512 / BNv;  // TMEM accumulator buffers
+    const uint32_t d = tmem + s.buf * (uint32_t)BNv;
     const uint64_t b0 = b_desc0 + (uint64_t)(s.stage * stage_step);
-    const uint32_t nbuf = s.buf ^ 1u;
+    const uint32_t nbuf = s.buf + 1u == kNB ? 0u : s.buf + 1u;
     int nstage = s.stage + 1;
     uint32_t nph = s.ph;
     if (nstage == p.stages) {
@@ -202,7 +203,7 @@ __device__ __forceinline__ void mma_item_waits(
         TR(2, s.tile_no + 1);
         fence_after();
       }
-      constexpr uint32_t kA = 128 * 128 >> 4, kB = 256 * 128 >> 4;
+      constexpr uint32_t kA = 128 * 128 >> 4, kB = BNv * 128 >> 4;
       umma_f16(d, a_desc0 + (uint64_t)((ks >> 2) * kA + (ks & 3) * 2),
                b0 + (uint64_t)((ks >> 2) * kB + (ks & 3) * 2), p.idesc,
                ks > 0 ? 1u : 0u);
@@ -340,8 +341,11 @@ struct Params {
 // clock under the cap); a B stage is refilled only when every CTA's MMAs
 // released it (empty barriers count kCS, commits multicast).  map_ph: the
 // point operand with 256/kCS-row boxes.
-template <bool kAStream, int kCS, int kQ>
-__global__ void __launch_bounds__(Epi<kQ>::kThreads, 1)
+// kBN: points per tile = TMEM columns per accumulator buffer; 512 / kBN
+// buffers.  256 (two buffers) in use; 128 (four buffers) is a timing
+// experiment (EXEM_TC_BN=128), measured slower at small d.
+template <bool kAStream, int kCS, int kQ, int kBN>
+__global__ void __launch_bounds__(Epi<kQ, kBN>::kThreads, 1)
     gains_tc_kernel(const __grid_constant__ CUtensorMap map_c,
                     const __grid_constant__ CUtensorMap map_p,
                     const __grid_constant__ CUtensorMap map_ph,
@@ -350,33 +354,35 @@ __global__ void __launch_bounds__(Epi<kQ>::kThreads, 1)
   // 1024-align the dynamic smem base (swizzle atoms).
   unsigned char *smem = (unsigned char *)(((uintptr_t)smem_raw + 1023) &
                                           ~(uintptr_t)1023);
+  constexpr int kBChunk = kBN * 128;   // bytes of one B K-chunk
+  constexpr int kNB = 512 / kBN;       // TMEM accumulator buffers
   const int a_bytes = kAStream ? 0 : p.kchunks * A_CHUNK;
   const int stage_bytes =
-      p.tile_stage ? p.kchunks * B_CHUNK : B_CHUNK + (kAStream ? A_CHUNK : 0);
+      p.tile_stage ? p.kchunks * kBChunk : kBChunk + (kAStream ? A_CHUNK : 0);
   unsigned char *sa = smem;                      // stationary A chunks
   unsigned char *sb = smem + a_bytes;            // stages
   uint64_t *bars = (uint64_t *)(sb + p.stages * stage_bytes);
   uint64_t *full = bars;                         // [stages]
   uint64_t *empty = bars + p.stages;             // [stages]
-  uint64_t *tfull = bars + 2 * p.stages;         // [2]
-  uint64_t *tempty = tfull + 2;                  // [2]
-  uint64_t *afull = tempty + 2;                  // [1]
+  uint64_t *tfull = bars + 2 * p.stages;         // [kNB]
+  uint64_t *tempty = tfull + kNB;                // [kNB]
+  uint64_t *afull = tempty + kNB;                // [1]
   uint64_t *aempty = afull + 1;                  // [1]
   uint32_t *tmem_slot = (uint32_t *)(aempty + 1);
   double *red = (double *)(tmem_slot + 4);       // [BM] half-merge buffer
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int kEpiCols = Epi<kQ>::kCols;
-  constexpr int kEpiWarps = Epi<kQ>::kWarps;
-  constexpr int kProdWarp = Epi<kQ>::kProdWarp;
-  constexpr int kMmaWarp = Epi<kQ>::kMmaWarp;
+  constexpr int kEpiCols = Epi<kQ, kBN>::kCols;
+  constexpr int kEpiWarps = Epi<kQ, kBN>::kWarps;
+  constexpr int kProdWarp = Epi<kQ, kBN>::kProdWarp;
+  constexpr int kMmaWarp = Epi<kQ, kBN>::kMmaWarp;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < p.stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kCS);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kNB; ++b) {
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], kEpiWarps);
     }
@@ -425,7 +431,7 @@ __global__ void __launch_bounds__(Epi<kQ>::kThreads, 1)
         }
         const int64_t p0 = sp * p.split_pts;
         const int64_t p1 = min(p.n, p0 + p.split_pts);
-        for (int64_t pt = p0; pt < p1; pt += BN) {
+        for (int64_t pt = p0; pt < p1; pt += kBN) {
           // whole-tile stages: one stage = every K chunk of the B tile
           const int per_stage = p.tile_stage ? p.kchunks : 1;
           for (int kc0 = 0; kc0 < p.kchunks; kc0 += per_stage) {
@@ -437,17 +443,17 @@ __global__ void __launch_bounds__(Epi<kQ>::kThreads, 1)
               // this CTA's 1/kCS of the B tile, to every CTA of the cluster
               mbar_expect_tx(&full[stage], (uint32_t)stage_bytes);
               for (int j = 0; j < per_stage; ++j)
-                tma_load_2d_mc(dst + j * B_CHUNK + crank * (B_CHUNK / kCS),
+                tma_load_2d_mc(dst + j * kBChunk + crank * (kBChunk / kCS),
                                &map_ph, &full[stage], (kc0 + j) * KCH,
-                               (int)(pt + crank * (BN / kCS)),
+                               (int)(pt + crank * (kBN / kCS)),
                                (uint16_t)((1u << kCS) - 1));
             } else {
               mbar_expect_tx(&full[stage], (uint32_t)stage_bytes);
               for (int j = 0; j < per_stage; ++j)
-                tma_load_2d(dst + j * B_CHUNK, &map_p, &full[stage],
+                tma_load_2d(dst + j * kBChunk, &map_p, &full[stage],
                             (kc0 + j) * KCH, (int)pt);
               if (kAStream)
-                tma_load_2d(dst + B_CHUNK, &map_c, &full[stage], kc0 * KCH,
+                tma_load_2d(dst + kBChunk, &map_c, &full[stage], kc0 * KCH,
                             crow);
             }
             if (++stage == p.stages) {
@@ -482,13 +488,13 @@ __global__ void __launch_bounds__(Epi<kQ>::kThreads, 1)
         const int64_t p1 = min(p.n, p0 + p.split_pts);
         if (p.tile_stage && p.ksteps <= 8 && !TC_PROBE_ANY(p, ~5)) {
           // software-pipelined handshake (see mma_item_waits)
-          const int ntiles = (int)((p1 - p0 + BN - 1) / BN);
+          const int ntiles = (int)((p1 - p0 + kBN - 1) / kBN);
           MmaState ms{stage, ph, tph, buf, tile_no};
           const uint32_t st_step = stage_step;
           switch (p.ksteps) {
 #define EXEM_K3_ITEM(K)                                                       \
   case K:                                                                     \
-    mma_item_waits<K, (K > 2 ? K - 2 : 0), (K > 1 ? K - 1 : 0), kCS>(        \
+    mma_item_waits<K, (K > 2 ? K - 2 : 0), (K > 1 ? K - 1 : 0), kCS, kBN>(   \
         p, ntiles, ms, a_desc0, b_desc0, st_step, tmem, full, empty, tfull,   \
         tempty);                                                              \
     break;
@@ -505,32 +511,32 @@ __global__ void __launch_bounds__(Epi<kQ>::kThreads, 1)
         }
         for (int64_t pt = p0;
              pt < p1 && !(p.tile_stage && p.ksteps <= 8 && !TC_PROBE_ANY(p, ~5));
-             pt += BN) {
+             pt += kBN) {
           TR(0, tile_no);
           mbar_wait(&tempty[buf], ((tph >> buf) & 1u) ^ 1u);
           TR(1, tile_no);
           tph ^= 1u << buf;
           fence_after();  // TMEM WAR vs the epilogue's tcgen05.ld
-          const uint32_t dcol = tmem + buf * (uint32_t)BN;
+          const uint32_t dcol = tmem + buf * (uint32_t)kBN;
           if (p.tile_stage) {
             if (!TC_PROBE(p, 8)) mbar_wait(&full[stage], ph);
             TR(2, tile_no);
             const uint64_t bd0 = b_desc0 + (uint64_t)((TC_PROBE(p, 128) ? 0 : stage) * stage_step);
             if (!TC_PROBE(p, 2)) {
               switch (p.ksteps) {  // compile-time K for d <= 122
-                case 1: issue_tile<1>(dcol, a_desc0, bd0, p.idesc); break;
-                case 2: issue_tile<2>(dcol, a_desc0, bd0, p.idesc); break;
-                case 3: issue_tile<3>(dcol, a_desc0, bd0, p.idesc); break;
-                case 4: issue_tile<4>(dcol, a_desc0, bd0, p.idesc); break;
-                case 5: issue_tile<5>(dcol, a_desc0, bd0, p.idesc); break;
-                case 6: issue_tile<6>(dcol, a_desc0, bd0, p.idesc); break;
-                case 7: issue_tile<7>(dcol, a_desc0, bd0, p.idesc); break;
-                case 8: issue_tile<8>(dcol, a_desc0, bd0, p.idesc); break;
+                case 1: issue_tile<1, kBN>(dcol, a_desc0, bd0, p.idesc); break;
+                case 2: issue_tile<2, kBN>(dcol, a_desc0, bd0, p.idesc); break;
+                case 3: issue_tile<3, kBN>(dcol, a_desc0, bd0, p.idesc); break;
+                case 4: issue_tile<4, kBN>(dcol, a_desc0, bd0, p.idesc); break;
+                case 5: issue_tile<5, kBN>(dcol, a_desc0, bd0, p.idesc); break;
+                case 6: issue_tile<6, kBN>(dcol, a_desc0, bd0, p.idesc); break;
+                case 7: issue_tile<7, kBN>(dcol, a_desc0, bd0, p.idesc); break;
+                case 8: issue_tile<8, kBN>(dcol, a_desc0, bd0, p.idesc); break;
                 default:
 #pragma unroll 1
                   for (int ks = 0; ks < p.ksteps; ++ks) {
                     const uint32_t off_a = (uint32_t)((ks >> 2) * (A_CHUNK >> 4) + (ks & 3) * 2);
-                    const uint32_t off_b = (uint32_t)((ks >> 2) * (B_CHUNK >> 4) + (ks & 3) * 2);
+                    const uint32_t off_b = (uint32_t)((ks >> 2) * (kBChunk >> 4) + (ks & 3) * 2);
                     umma_f16(dcol, a_desc0 + off_a, bd0 + off_b, p.idesc,
                              ks > 0 ? 1u : 0u);
                   }
@@ -552,7 +558,7 @@ __global__ void __launch_bounds__(Epi<kQ>::kThreads, 1)
               if (kc == 0) TR(2, tile_no);
               const uint64_t bd = b_desc0 + (uint64_t)(stage * stage_step);
               const uint64_t ad =
-                  kAStream ? bd + (uint64_t)(B_CHUNK >> 4)
+                  kAStream ? bd + (uint64_t)(kBChunk >> 4)
                            : a_desc0 + (uint64_t)(kc * (A_CHUNK >> 4));
               const int nk = ks_left < KCH / 16 ? ks_left : KCH / 16;
               if (!TC_PROBE(p, 2)) {
@@ -586,7 +592,7 @@ __global__ void __launch_bounds__(Epi<kQ>::kThreads, 1)
           umma_commit(&tfull[buf]);
           TR(3, tile_no);
           ++tile_no;
-          buf ^= 1u;
+          buf = buf + 1u == (uint32_t)kNB ? 0u : buf + 1u;
         }
         if (!kAStream) umma_commit(aempty);
       }
@@ -608,7 +614,7 @@ __global__ void __launch_bounds__(Epi<kQ>::kThreads, 1)
       const int64_t p0 = sp * p.split_pts;
       const int64_t p1 = min(p.n, p0 + p.split_pts);
       double g = 0.0;
-      for (int64_t pt = p0; pt < p1; pt += BN) {
+      for (int64_t pt = p0; pt < p1; pt += kBN) {
         if (tr) TR(4, tile_no);
         // one lane polls the barrier; the warp sync orders the others
         if (lane == 0) {
@@ -626,10 +632,10 @@ __global__ void __launch_bounds__(Epi<kQ>::kThreads, 1)
         tph ^= 1u << buf;
         fence_after();
         const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) +
-                               (uint32_t)(buf * BN + grp * kEpiCols);
+                               (uint32_t)(buf * kBN + grp * kEpiCols);
         // Drain this warp's 32 x kEpiCols slice of the accumulator into
         // registers first and release the TMEM buffer immediately, so the
-        // MMA of tile t+2 never waits on this tile's arithmetic.
+        // MMA of tile t+kNB never waits on this tile's arithmetic.
         uint32_t r[kEpiCols / 32][32];
 #pragma unroll
         for (int c = 0; c < kEpiCols / 32; ++c) TMEM_LD32(taddr + 32 * c, r[c]);
@@ -640,7 +646,7 @@ __global__ void __launch_bounds__(Epi<kQ>::kThreads, 1)
         if (tr) TR(6, tile_no);
         if (TC_PROBE(p, 1)) {  // timing experiment: no epilogue arithmetic
           g += (double)__uint_as_float(r[0][0] ^ r[kEpiCols / 32 - 1][31]);
-          buf ^= 1u;
+          buf = buf + 1u == (uint32_t)kNB ? 0u : buf + 1u;
           ++tile_no;
           continue;
         }
@@ -682,7 +688,7 @@ __global__ void __launch_bounds__(Epi<kQ>::kThreads, 1)
 #endif
         if (tr) TR(7, tile_no);
         ++tile_no;
-        buf ^= 1u;
+        buf = buf + 1u == (uint32_t)kNB ? 0u : buf + 1u;
       }
       // fixed-order merge of the column groups: ((g0 + g1) + g2) + g3
       // through one [BM] buffer
@@ -930,7 +936,6 @@ int exem_greedy_gains_tc_ex(int dtype, const void *xc, int64_t l,
   prm.cand_tiles = ceil_div(l, BM);
   prm.ksteps = ksteps;
   prm.kchunks = kchunks;
-  prm.idesc = make_idesc(dtype == EXEM_BF16, BM, BN);
   prm.partial = partial;
   prm.hits = screen_hits;
   {
@@ -951,8 +956,18 @@ int exem_greedy_gains_tc_ex(int dtype, const void *xc, int64_t l,
   // Whole-tile stages (one barrier handshake per B tile) when >= 3 fit.
   const bool tile_stage =
       !astream && (avail - kchunks * A_CHUNK) / (kchunks * B_CHUNK) >= 3;
-  const int stage_bytes = tile_stage ? kchunks * B_CHUNK
-                                     : B_CHUNK + (astream ? A_CHUNK : 0);
+  // 256-point tiles in two TMEM buffers.  EXEM_TC_BN = 128 (timing
+  // experiments, whole-tile stages only) runs 128-point tiles in four
+  // buffers: measured slower even at d = 2 / 16 / 20 (1.92 / 2.02 / 2.02 vs
+  // 1.51 / 1.53 / 1.53 ms per C3 step) -- the per-tile epilogue cost, not
+  // the two-buffer release chain, bounds the small-d tiles.
+  int bn = BN;
+  if (const char *eb = getenv("EXEM_TC_BN"))
+    if (tile_stage && !astream && atoi(eb) == 128) bn = 128;
+  prm.idesc = make_idesc(dtype == EXEM_BF16, BM, bn);
+  const int b_chunk = bn * 128;
+  const int stage_bytes = tile_stage ? kchunks * b_chunk
+                                     : b_chunk + (astream ? A_CHUNK : 0);
   int stages = (avail - (astream ? 0 : kchunks * A_CHUNK)) / stage_bytes;
   if (stages > 8) stages = 8;
   if (const char *ms = getenv("EXEM_TC_STAGES")) stages = atoi(ms);  // timing only
@@ -962,32 +977,35 @@ int exem_greedy_gains_tc_ex(int dtype, const void *xc, int64_t l,
                       (size_t)stages * stage_bytes + kBarBytes + 1024;
   CUtensorMap mc, mp;
   if (int rc = make_map(&mc, xc, dtype, exem_tc_rows(l), kp, BM)) return rc;
-  if (int rc = make_map(&mp, xp, dtype, exem_tc_rows(n), kp, BN)) return rc;
+  if (int rc = make_map(&mp, xp, dtype, exem_tc_rows(n), kp, bn)) return rc;
   // clusters sharing B tiles by TMA multicast (whole-tile stages, the
   // pipelined issuer): cluster size 2 by default, EXEM_TC_MC = 0 | 1 | 2 | 4
   // (0/1: none) for timing experiments
   int cs = (tile_stage && !astream && ksteps <= 8 && prm.dbg == 0) ? 2 : 1;
   if (const char *e = getenv("EXEM_TC_MC"))
     if (cs > 1) cs = atoi(e) >= 4 ? 4 : (atoi(e) >= 2 ? 2 : 1);
+  if (bn != BN && cs > 2) cs = 2;  // the narrow tiles have pairs only
   const bool mcast = cs > 1;
-  CUtensorMap mph;  // 256/cs-row boxes: one CTA's share of a B tile
-  if (int rc = make_map(&mph, xp, dtype, exem_tc_rows(n), kp, BN / cs))
+  CUtensorMap mph;  // bn/cs-row boxes: one CTA's share of a B tile
+  if (int rc = make_map(&mph, xp, dtype, exem_tc_rows(n), kp, bn / cs))
     return rc;
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e;
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute at[1];
-  cfg.blockDim = dim3(q == 4 ? Epi<4>::kThreads : Epi<2>::kThreads);
+  cfg.blockDim = dim3(q == 4 ? Epi<4>::kThreads : Epi<2>::kThreads);  // any BN
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  // one kernel instantiation per (A streamed, cluster size, Q)
+  // one kernel instantiation per (A streamed, cluster size, Q, tile width)
   auto pick = [&](bool as, int c) {
-#define EXEM_K3_PICK(AS, CS)                                                  \
-  (q == 4 ? gains_tc_kernel<AS, CS, 4> : gains_tc_kernel<AS, CS, 2>)
-    return as ? EXEM_K3_PICK(true, 1)
-              : (c == 4 ? EXEM_K3_PICK(false, 4)
-                        : (c == 2 ? EXEM_K3_PICK(false, 2)
-                                  : EXEM_K3_PICK(false, 1)));
+#define EXEM_K3_PICK(AS, CS, B)                                               \
+  (q == 4 ? gains_tc_kernel<AS, CS, 4, B> : gains_tc_kernel<AS, CS, 2, B>)
+    if (bn == 128)
+      return c == 2 ? EXEM_K3_PICK(false, 2, 128) : EXEM_K3_PICK(false, 1, 128);
+    return as ? EXEM_K3_PICK(true, 1, BN)
+              : (c == 4 ? EXEM_K3_PICK(false, 4, BN)
+                        : (c == 2 ? EXEM_K3_PICK(false, 2, BN)
+                                  : EXEM_K3_PICK(false, 1, BN)));
 #undef EXEM_K3_PICK
   };
   auto kern = pick(astream, cs);

@@ -405,3 +405,28 @@ def test_point_loss_decomposition_within_fp64_bound():
         parts = np.array([pb.point_loss(g, i, elems) for i in range(50)])
         whole = pb.kmedoids_loss(g, np.vstack([elems, np.zeros((1, 4))]))
         assert abs(float(np.sum(parts)) - whole) <= 1e-12 * max(1.0, abs(whole))
+
+
+@pytest.mark.parametrize("prec", [BF16, P16])
+@pytest.mark.parametrize("d", [2, 8, 16, 26, 27])
+@pytest.mark.parametrize("bn", ["256", "128"])
+def test_tc_greedy_small_d(prec, d, bn, monkeypatch):
+    """Small d: one or two K = 16 MMAs per tile (d <= 26; d = 27 is the
+    first three-step shape), with the shipped 256-point tiles and the
+    128-point / four-TMEM-buffer experiment layout (EXEM_TC_BN = 128), both
+    teacher-forced against fp64 truth, with the epilogue width chosen per
+    run (clustered data makes the screens fire)."""
+    if bn != "256":
+        monkeypatch.setenv("EXEM_TC_BN", bn)
+    rng = np.random.default_rng(d)
+    n, k = 5000, 6
+    centres = rng.standard_normal((8, d)) * 3.0
+    data = centres[rng.integers(0, 8, n)] + rng.standard_normal((n, d))
+    data *= 0.5 if prec is P16 else 1.0
+    g = pb.build_ground_set(data, precision=prec)
+    res = pb.greedy_maximize(g, k=k)
+    slack = 2 * ulp32(g.aux_loss)
+    teacher_forced_trajectory(
+        g, res, lambda G: HALF_G_REL * max(1.0, abs(G)),
+        lambda f: HALF_F_REL * max(1.0, abs(f)) + slack,
+        label=f"K3-TC small d={d} {prec.name} bn={bn}")
