@@ -183,7 +183,12 @@ def device_set_min(ground: GroundSet, elems: np.ndarray, include_aux: bool,
         en = t.empty(max(k, 1), dtype=t.float64, device=dg.dev)
         if k:
             lib.row_norms(prec.tag, N.ptr(e), k, dg.d, dg.d_pad, N.ptr(en), st)
-        t_out = t.empty(dg.n, dtype=dg.vt.dtype, device=dg.dev) if want_t else None
+        # sets larger than one element group of the TMA K2 (64 at 4-byte,
+        # 32 at 8-byte compute types) carry the running minimum through
+        # t_out: give it one even when only the sum is wanted
+        groups = k > (32 if dg.vt.element_size() == 8 else 64)
+        t_out = (t.empty(dg.n, dtype=dg.vt.dtype, device=dg.dev)
+                 if want_t or groups else None)
         lab = t.empty(dg.n, dtype=t.int64, device=dg.dev) if want_labels else None
         s = t.empty(1, dtype=t.float64, device=dg.dev)
         lib.set_min(prec.tag, N.ptr(dg.vt), dg.ld, dg.n, dg.d, N.ptr(dg.norms),

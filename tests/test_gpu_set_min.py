@@ -112,3 +112,13 @@ def test_set_min_deterministic_and_streamed_equal():
         a = pb.evaluate_single(g, elems)
         assert pb.evaluate_single(g, elems) == a
         assert pb.evaluate_single(gs, elems) == a
+
+
+@pytest.mark.parametrize("n,d", [(1, 1), (2, 3), (255, 8), (256, 5), (257, 17),
+                                 (513, 2)])
+@pytest.mark.parametrize("k", [1, 3, 20])
+def test_set_min_tiny_shapes(n, d, k):
+    """Ragged last tiles, n below one 256-point tile, d = 1."""
+    k = min(k, n)
+    g, og, idx = _case(P32, n, d, k, seed=n * 31 + d + k)
+    _check(g, og, idx, P32)

@@ -103,17 +103,24 @@ def main():
             n * d * prec.bytes_per_value + n * dg.d_pad * 4 + 16 * n, t)
         if prec is not pb.Precision.binary32:
             continue
-        for k in (1, 10, 16, 50, 64, 100):
+        for k in (1, 10, 16, 50, 64, 100, 128):
             elems = padded_rows(g.matrix[:k], dg.d_pad, prec, dg.dev)
             en = torch.empty(k, dtype=torch.float64, device=dg.dev)
             lib.row_norms(prec.tag, N.ptr(elems), k, d, dg.d_pad, N.ptr(en), st)
             s = torch.empty(1, dtype=torch.float64, device=dg.dev)
+            # k > 64: several element groups, the running minimum carried in
+            # t_out (as objective.device_set_min does)
+            tb = (torch.empty(n, dtype=torch.float32, device=dg.dev)
+                  if k > 64 else None)
             t = timed(lambda: lib.set_min(
                 prec.tag, N.ptr(dg.vt), dg.ld, n, d, N.ptr(dg.norms),
-                N.ptr(dg.aux), N.ptr(elems), N.ptr(en), k, 1, None, None,
+                N.ptr(dg.aux), N.ptr(elems), N.ptr(en), k, 1, N.ptr(tb), None,
                 N.ptr(s), N.ptr(dg.scratch), st))
+            groups = -(-k // 64)  # V passes (element groups of 64)
             rec(f"K2 set_min k={k} (single-set evaluate)",
-                n * d * 4 + 12 * n + k * d * 4, t, 2.0 * n * k * d)
+                groups * n * d * 4 + 12 * n + k * d * 4 +
+                (8 * n * (2 * groups - 1) if k > 64 else 0), t,
+                2.0 * n * k * d)
         # assign_clusters: K2 with the argmin-label epilogue, k = 50 exemplars
         elems = padded_rows(g.matrix[:50], dg.d_pad, prec, dg.dev)
         en = torch.empty(50, dtype=torch.float64, device=dg.dev)
