@@ -41,6 +41,17 @@ extern "C" {
 #define EXEM_F32 2
 #define EXEM_F64 3
 
+/* OR'd into the dtype tag of the entry points that take the column-major
+ * V buffer `vt` (exem_ground_prepare[_rows] as output; exem_set_min,
+ * exem_greedy_update (vt and cvt), exem_tc_pack_candidates/_points/
+ * _points_plain as input): for bf16/f16 ground sets `vt` holds the 2-byte
+ * STORAGE values instead of their binary32 widening -- half the HBM bytes
+ * of K1/K2/the m-update and one fewer 4-byte copy of V.  Arithmetic is
+ * unchanged (values are widened in registers), so results are bit-identical
+ * to the widened layout.  Rejected (EXEM_ERR_ARG) with f32/f64 tags and by
+ * entry points that do not list it. */
+#define EXEM_VT_STORAGE 0x100
+
 /* ---- status codes -> pkg/src/exembatch/errors.py:4-41 ---- */
 #define EXEM_OK 0
 #define EXEM_ERR_ARG 1         /* ValueError / DimensionMismatchError        */
@@ -50,7 +61,7 @@ extern "C" {
 #define EXEM_ERR_UNSUPPORTED 5 /* ExemError: no sm_100a device / bad dtype   */
 
 const char *exem_last_error(void);
-int exem_abi_version(void); /* 3: exem_greedy_gains_tc_ex (2: check_finite in K1, interleaved K4-TC set tiles) */
+int exem_abi_version(void); /* 4: EXEM_VT_STORAGE (2-byte vt); 3: exem_greedy_gains_tc_ex (2: check_finite in K1, interleaved K4-TC set tiles) */
 
 /* Device query: SM count, compute capability, opt-in shared memory. */
 int exem_device_info(int device, int *sm_count, int *cc_major, int *cc_minor,
@@ -134,6 +145,10 @@ int exem_h2d_bytes(void *dst, const void *host, int64_t bytes, void *stream);
  *            (assign_clusters, pkg/src/exembatch/optimize.py:115-136).
  *   sum_out  optional [1] double fixed-order sum_i t_i.
  */
+/* 1 when exem_set_min runs (dtype | EXEM_VT_STORAGE) for this shape (the
+ * TMA-fed K2; the cp.async K2 reads widened vt only); has_t_out: a t_out
+ * buffer will be passed (needed when k exceeds one element group). */
+int exem_set_min_storage_ok(int dtype, int64_t d, int64_t k, int has_t_out);
 int exem_set_min(int dtype, const void *vt, int64_t ld, int64_t n, int64_t d,
                  const double *norms, const void *aux, const void *elems,
                  const double *enorms, int64_t k, int include_aux, void *t_out,

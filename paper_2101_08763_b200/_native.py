@@ -25,6 +25,8 @@ LIB_PATH = Path(__file__).resolve().parent / "libexem_b200.so"
 
 # dtype tags (include/exem_b200.h)
 F16, BF16, F32, F64 = 0, 1, 2, 3
+# OR'd into a half tag: the vt buffer holds 2-byte storage values
+VT_STORAGE = 0x100
 
 # status codes -> reference exception classes (pkg/src/exembatch/errors.py)
 OK, ERR_ARG, ERR_OOM, ERR_CUDA, ERR_DATA, ERR_UNSUPPORTED = range(6)
@@ -43,6 +45,7 @@ _SIGNATURES = {
     "exem_reduce_scratch": (c_int64, [c_int64]),
     "exem_ground_prepare": (c_int, [c_int, _P, c_int64, c_int64, _P, _P,
                                     c_int64, _P, _P, _P, _P, c_int, _P]),
+    "exem_set_min_storage_ok": (c_int, [c_int, c_int64, c_int64, c_int]),
     "exem_set_min": (c_int, [c_int, _P, c_int64, c_int64, c_int64, _P, _P, _P,
                              _P, c_int64, c_int, _P, _P, _P, _P, _P]),
     "exem_batch_eval": (c_int, [c_int, _P, c_int64, c_int64, c_int64, _P, _P,
@@ -141,7 +144,8 @@ class _Lib:
 
     def __getattr__(self, name):
         fn = getattr(self._h, "exem_" + name)
-        if fn.restype is not c_int or name in ("abi_version",):
+        if fn.restype is not c_int or name in ("abi_version",
+                                               "set_min_storage_ok"):
             return fn
 
         def call(*args):
@@ -165,8 +169,9 @@ def raise_status(rc: int, msg: str):
 
 # Bumped whenever an entry point's signature or contract changes
 # (2: exem_ground_prepare[_rows] gained check_finite; K4-TC set tiles are
-# column-interleaved; 3: exem_greedy_gains_tc_ex).
-ABI_VERSION = 3
+# column-interleaved; 3: exem_greedy_gains_tc_ex; 4: EXEM_VT_STORAGE,
+# exem_set_min_storage_ok).
+ABI_VERSION = 4
 
 
 def load_library(path: Path | str | None = None) -> _Lib:

@@ -85,6 +85,27 @@ template <> __device__ __forceinline__ double from_d<double>(double x) {
   return x;
 }
 
+// ------------------------------------------- vt element type
+// vt holds the compute type, or (dtype | EXEM_VT_STORAGE, half tags only)
+// the 2-byte storage values themselves; kernels widen in registers.
+template <int DT, bool VS> struct VtOf {
+  using T = typename Traits<DT>::C;
+};
+template <> struct VtOf<EXEM_F16, true> { using T = __half; };
+template <> struct VtOf<EXEM_BF16, true> { using T = __nv_bfloat16; };
+
+// exact narrowing of a value that came from the storage type
+template <typename T> __device__ __forceinline__ T to_vt(float x);
+template <> __device__ __forceinline__ float to_vt<float>(float x) { return x; }
+template <> __device__ __forceinline__ __half to_vt<__half>(float x) {
+  return __float2half_rn(x);
+}
+template <> __device__ __forceinline__ __nv_bfloat16 to_vt<__nv_bfloat16>(float x) {
+  return __float2bfloat16_rn(x);
+}
+template <typename T> __device__ __forceinline__ T to_vt(double x);
+template <> __device__ __forceinline__ double to_vt<double>(double x) { return x; }
+
 template <typename T> __device__ __forceinline__ T tmax(T a, T b);
 template <> __device__ __forceinline__ float tmax(float a, float b) {
   return fmaxf(a, b);
@@ -176,6 +197,38 @@ template <int N> __device__ __forceinline__ void cp_async_wait() {
 
 // Dispatch a dtype tag to a template body (no runtime multi-backend: one
 // kernel instantiation per precision).
+// EXEM_DISPATCH plus the vt element flag: VS is a constexpr bool (true only
+// for a half tag carrying EXEM_VT_STORAGE)
+#define EXEM_DISPATCH_VT(dtype, DT, VS, ...)                                   \
+  do {                                                                         \
+    const int _tag = (int)(dtype) & ~EXEM_VT_STORAGE;                          \
+    const bool _vs = ((int)(dtype) & EXEM_VT_STORAGE) != 0;                    \
+    if (_vs && _tag != EXEM_F16 && _tag != EXEM_BF16)                          \
+      return ::exem::fail(EXEM_ERR_ARG,                                        \
+                          "EXEM_VT_STORAGE needs a bf16/f16 tag (got %d)",     \
+                          _tag);                                               \
+    switch (_tag) {                                                            \
+      case EXEM_F16:                                                           \
+        if (_vs) { constexpr int DT = EXEM_F16; constexpr bool VS = true;      \
+                   __VA_ARGS__; }                                              \
+        else { constexpr int DT = EXEM_F16; constexpr bool VS = false;         \
+               __VA_ARGS__; }                                                  \
+        break;                                                                 \
+      case EXEM_BF16:                                                          \
+        if (_vs) { constexpr int DT = EXEM_BF16; constexpr bool VS = true;     \
+                   __VA_ARGS__; }                                              \
+        else { constexpr int DT = EXEM_BF16; constexpr bool VS = false;        \
+               __VA_ARGS__; }                                                  \
+        break;                                                                 \
+      case EXEM_F32: { constexpr int DT = EXEM_F32; constexpr bool VS = false; \
+                       __VA_ARGS__; break; }                                   \
+      case EXEM_F64: { constexpr int DT = EXEM_F64; constexpr bool VS = false; \
+                       __VA_ARGS__; break; }                                   \
+      default:                                                                 \
+        return ::exem::fail(EXEM_ERR_ARG, "unknown dtype tag %d", _tag);       \
+    }                                                                          \
+  } while (0)
+
 #define EXEM_DISPATCH(dtype, DT, ...)                                          \
   switch (dtype) {                                                             \
     case EXEM_F16: { constexpr int DT = EXEM_F16; __VA_ARGS__; break; }        \

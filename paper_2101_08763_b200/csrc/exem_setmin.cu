@@ -47,9 +47,44 @@ constexpr int kStageBytes = 8 * 1024;
 constexpr int kElemSmemMax = 128 * 1024;  // resident element budget
 constexpr int kSmemPerSm = 227 * 1024;
 
-// dimensions per ring stage (8 KB of V): exactly d_pad = round_up(d, 8)
-// dimensions are streamed (no dead FMAs on padding chunks)
-template <typename C> constexpr int bk_of() { return kStageBytes / (kP * (int)sizeof(C)); }
+// dimensions per ring stage (8 KB of 4/8-byte V): exactly d_pad =
+// round_up(d, 8) dimensions are streamed (no dead FMAs on padding chunks);
+// 2-byte storage-typed V (EXEM_VT_STORAGE) keeps 8 dimensions in 4 KB stages
+template <typename V> constexpr int bk_of() {
+  return sizeof(V) == 2 ? 8 : kStageBytes / (kP * (int)sizeof(V));
+}
+template <typename V> constexpr int stage_bytes() {
+  return bk_of<V>() * kP * (int)sizeof(V);
+}
+
+// PT consecutive storage-typed points of one dimension, widened (one
+// 4/8/16-byte shared load per 2/4/8 points)
+template <typename V, int PT, typename C>
+__device__ __forceinline__ void load_pts(const V *p, C (&pv)[PT]) {
+  constexpr int bytes = PT * (int)sizeof(V);
+  if constexpr (bytes == 2) {
+    pv[0] = to_c(p[0]);
+  } else if constexpr (bytes == 4) {
+    const uint32_t raw = *reinterpret_cast<const uint32_t *>(p);
+    const V *q = reinterpret_cast<const V *>(&raw);
+#pragma unroll
+    for (int w = 0; w < PT; ++w) pv[w] = to_c(q[w]);
+  } else if constexpr (bytes == 8) {
+    const uint2 raw = *reinterpret_cast<const uint2 *>(p);
+    const V *q = reinterpret_cast<const V *>(&raw);
+#pragma unroll
+    for (int w = 0; w < PT; ++w) pv[w] = to_c(q[w]);
+  } else {
+    constexpr int per = 16 / (int)sizeof(V);
+#pragma unroll
+    for (int u = 0; u < PT; u += per) {
+      const uint4 raw = *reinterpret_cast<const uint4 *>(p + u);
+      const V *q = reinterpret_cast<const V *>(&raw);
+#pragma unroll
+      for (int w = 0; w < per; ++w) pv[u + w] = to_c(q[w]);
+    }
+  }
+}
 
 template <typename C> struct Vec4;
 template <> struct Vec4<float> {
@@ -106,7 +141,7 @@ __device__ __forceinline__ void combine_tile(double (&wsum)[2][kWarps],
 template <int EG>
 constexpr int min_ctas() { return EG == 1 ? 4 : (EG == 2 ? 3 : 2); }
 
-template <int DT, int EG, int ET>
+template <int DT, int EG, int ET, bool VS>
 __global__ void __launch_bounds__(kThreads, min_ctas<EG>())
     set_min_tma_kernel(const __grid_constant__ CUtensorMap vmap,
                        int64_t n, int d_pad, int nstages,
@@ -121,7 +156,8 @@ __global__ void __launch_bounds__(kThreads, min_ctas<EG>())
                        typename Traits<DT>::C *__restrict__ dist_out,
                        int64_t ldd) {
   using C = typename Traits<DT>::C;
-  constexpr int BK = bk_of<C>();
+  using VT = typename VtOf<DT, VS>::T;  // element type of the V stages
+  constexpr int BK = bk_of<VT>();
   constexpr int PT = EG;              // points per thread
   constexpr int KG = EG * ET;         // elements per group
   constexpr int ROW = EG * 8;         // smem values per dimension
@@ -130,8 +166,8 @@ __global__ void __launch_bounds__(kThreads, min_ctas<EG>())
   // HBM-bound shapes: fetch norms / aux of the tile before its chunk loop
   constexpr bool kPrefetch = PT <= 4;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  C *sv = reinterpret_cast<C *>(smem_raw);          // [S][BK][kP]
-  C *se = sv + nstages * STAGE;                     // [d_pad][EG][8]
+  VT *sv = reinterpret_cast<VT *>(smem_raw);        // [S][BK][kP]
+  C *se = reinterpret_cast<C *>(sv + nstages * STAGE);  // [d_pad][EG][8]
   __shared__ __align__(8) uint64_t full[kMaxStages];
   __shared__ uint32_t rel[kMaxStages];  // warps done with a stage's use
   __shared__ __align__(8) uint64_t wfull[2], wempty[2];
@@ -171,7 +207,7 @@ __global__ void __launch_bounds__(kThreads, min_ctas<EG>())
     const uint32_t within = ev % (uint32_t)(my_tiles * nchunks);
     const int64_t tile = blockIdx.x + (int64_t)(within / nchunks) * gridDim.x;
     const int c = (int)(within % nchunks);
-    tc::mbar_expect_tx(&full[s], (uint32_t)(STAGE * sizeof(C)));
+    tc::mbar_expect_tx(&full[s], (uint32_t)(STAGE * sizeof(VT)));
     tc::tma_load_2d(sv + s * STAGE, &vmap, &full[s], (int)(tile * kP), c * BK);
   };
   if (threadIdx.x == 0)
@@ -215,14 +251,16 @@ __global__ void __launch_bounds__(kThreads, min_ctas<EG>())
         // suspend in hardware until the box lands (a spin loop's
         // SYNCS/BRA/ISETP/YIELD were ~15 % of the issued instructions)
         tc::mbar_wait_hint(&full[s], (ev_use / nstages) & 1);
-        const C *cv = sv + s * STAGE + pg * PT;
+        const VT *cv = sv + s * STAGE + pg * PT;
         const C *ce = se + (c * BK) * ROW + eg * 8;
 #pragma unroll(kUnrollKK)
         for (int kk = 0; kk < BK; ++kk) {
           C pv[PT], ev[8];
           using V4 = typename Vec4<C>::T;
           constexpr int per = 16 / sizeof(C);
-          if constexpr (PT == 1) {
+          if constexpr (VS) {
+            load_pts<VT, PT, C>(cv + kk * kP, pv);
+          } else if constexpr (PT == 1) {
             pv[0] = cv[kk * kP];
           } else if constexpr (PT * sizeof(C) == 8) {
             const float2 q = *reinterpret_cast<const float2 *>(cv + kk * kP);
@@ -358,7 +396,7 @@ __global__ void __launch_bounds__(kThreads, min_ctas<EG>())
   }
 }
 
-template <int DT, int EG, int ET>
+template <int DT, int EG, int ET, bool VS>
 cudaError_t launch_t(const CUtensorMap &map, int64_t tiles, int sms,
                      cudaStream_t st, int64_t n, int d_pad,
                      const double *norms, const void *aux, const void *elems,
@@ -366,38 +404,43 @@ cudaError_t launch_t(const CUtensorMap &map, int64_t tiles, int sms,
                      void *t_out, int64_t *label_out, double *partials,
                      void *dist_out, int64_t ldd) {
   using C = typename Traits<DT>::C;
+  using VT = typename VtOf<DT, VS>::T;
+  constexpr size_t sb = (size_t)stage_bytes<VT>();
   const size_t elem_bytes = (size_t)d_pad * EG * 8 * sizeof(C);
   // 8 KB stages: 5 / 6 / 8 per CTA at 4 / 3 / 2 CTAs per SM (about
   // 130-170 KB in flight per SM); deeper rings with fewer CTAs measured
-  // slower (13 stages at 2 CTAs: 0.150 vs 0.084 ms at k = 1)
+  // slower (13 stages at 2 CTAs: 0.150 vs 0.084 ms at k = 1).  The 4 KB
+  // stages of 2-byte V keep the same bytes in flight with twice the count.
   int nst = EG == 1 ? 5 : (EG == 2 ? 6 : 8);
-  size_t smem = (size_t)nst * kStageBytes + elem_bytes;
+  if (sizeof(VT) == 2) nst *= 2;
+  if (nst > kMaxStages) nst = kMaxStages;
+  size_t smem = (size_t)nst * sb + elem_bytes;
   while (smem + 4096 > (size_t)kSmemPerSm && nst > 2) {
     --nst;
-    smem -= kStageBytes;
+    smem -= sb;
   }
   if (const char *ev = getenv("EXEM_K2_STAGES")) {  // timing experiments only
     const int want = atoi(ev);
     if (want >= 2 && want <= kMaxStages &&
-        (size_t)want * kStageBytes + elem_bytes + 4096 <= (size_t)kSmemPerSm) {
+        (size_t)want * sb + elem_bytes + 4096 <= (size_t)kSmemPerSm) {
       nst = want;
-      smem = (size_t)nst * kStageBytes + elem_bytes;
+      smem = (size_t)nst * sb + elem_bytes;
     }
   }
   cudaError_t e = cudaFuncSetAttribute(
-      set_min_tma_kernel<DT, EG, ET>,
+      set_min_tma_kernel<DT, EG, ET, VS>,
       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 1;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-          &per_sm, set_min_tma_kernel<DT, EG, ET>, kThreads, smem) !=
+          &per_sm, set_min_tma_kernel<DT, EG, ET, VS>, kThreads, smem) !=
           cudaSuccess || per_sm < 1)
     per_sm = 1;
   if (const char *ev = getenv("EXEM_K2_MAXCTA"))  // timing experiments only
     if (atoi(ev) >= 1 && atoi(ev) < per_sm) per_sm = atoi(ev);
   const int grid = (int)(tiles < (int64_t)per_sm * sms ? tiles
                                                        : (int64_t)per_sm * sms);
-  set_min_tma_kernel<DT, EG, ET><<<grid, kThreads, smem, st>>>(
+  set_min_tma_kernel<DT, EG, ET, VS><<<grid, kThreads, smem, st>>>(
       map, n, d_pad, nst, norms, (const C *)aux, (const C *)elems, enorms, k,
       include_aux, (C *)t_out, label_out, partials, (C *)dist_out, ldd);
   return cudaGetLastError();
@@ -413,19 +456,40 @@ int sm_count() {
 }
 
 // (EG, ET) for k elements: the fewest lanes per point whose 8-element rows
-// cover k (EG <= 8, <= 4 at f64), then ET = ceil(k / EG); half-storage sets
-// (direct form, twice the FMA work) use 8-wide rows only.
-void choose(int dtype, int k, int &eg, int &et) {
+// cover k (EG <= 8, <= 4 at f64), then ET = ceil(k / EG).
+void choose(int dtype, int k, int &eg, int &et, bool vs) {
   const int egmax = dtype == EXEM_F64 ? 4 : 8;
   eg = 1;
   while (eg < egmax && eg * 8 < k) eg *= 2;
   et = (k + eg - 1) / eg;
   if (et > 8) et = 8;  // several element groups
-  if (dtype == EXEM_F16 || dtype == EXEM_BF16) et = 8;
+  // widened half storage (the streamed slots): 8-wide rows only; 2-byte
+  // storage has the binary32 thread layouts (no dead element columns)
+  if ((dtype == EXEM_F16 || dtype == EXEM_BF16) && !vs) et = 8;
   if (eg > 1 && et < 5) et = 5;  // instantiated ET range for EG > 1
 }
 
+// the TMA kernel runs this shape: the element group fits the resident
+// budget and a multi-group set has its t_out carry
+bool set_min_tma_covers(int dtype, int d_pad, int k, bool has_t_out, bool vs) {
+  if (k < 1 || d_pad % 8 != 0) return false;
+  const int eb = dtype == EXEM_F64 ? 8 : 4;  // resident elements: compute type
+  int eg, et;
+  choose(dtype, k, eg, et, vs);
+  if (k > eg * et && !has_t_out) return false;
+  return (size_t)d_pad * eg * 8 * eb <= (size_t)kElemSmemMax;
+}
+
 }  // namespace
+
+int set_min_storage_ok(int dtype, int64_t d, int64_t k, int has_t_out) {
+  const int tag = dtype & ~EXEM_VT_STORAGE;
+  if (tag != EXEM_F16 && tag != EXEM_BF16) return 0;
+  if (k < 1 || k > (1 << 30) || d < 1) return 0;
+  if (!tc::get_encode()) return 0;
+  return set_min_tma_covers(tag, (int)round_up(d, kDimPad), (int)k,
+                            has_t_out != 0, true) ? 1 : 0;
+}
 
 // Returns 1 if the shape is not covered (caller uses the cp.async K2),
 // 0 on launch, or a negative CUDA error.  k > EG*ET runs several element
@@ -435,15 +499,16 @@ int set_min_tma(int dtype, const void *vt, int64_t ld, int64_t n, int d_pad,
                 const double *enorms, int k, int include_aux, void *t_out,
                 int64_t *label_out, double *partials, void *dist_out,
                 int64_t ldd, cudaStream_t st) {
+  const bool vs = (dtype & EXEM_VT_STORAGE) != 0;
+  dtype &= ~EXEM_VT_STORAGE;
+  if (vs && dtype != EXEM_F16 && dtype != EXEM_BF16) return 1;
   if (k < 1 || n < 1 || ld % kP != 0) return 1;
+  if (!set_min_tma_covers(dtype, d_pad, k, t_out != nullptr, vs)) return 1;
   const bool f64 = dtype == EXEM_F64;
-  const int vb = f64 ? 8 : 4;
-  const int bk = f64 ? bk_of<double>() : bk_of<float>();
-  if (d_pad % bk != 0) return 1;
+  const int vb = f64 ? 8 : (vs ? 2 : 4);  // bytes per V value
+  const int bk = f64 ? bk_of<double>() : (vs ? bk_of<__half>() : bk_of<float>());
   int eg, et;
-  choose(dtype, k, eg, et);
-  if (k > eg * et && !t_out) return 1;  // multi-group needs the t_out carry
-  if ((size_t)d_pad * eg * 8 * vb > (size_t)kElemSmemMax) return 1;
+  choose(dtype, k, eg, et, vs);
   CUtensorMap map;
   auto enc = tc::get_encode();
   if (!enc) return 1;
@@ -451,9 +516,12 @@ int set_min_tma(int dtype, const void *vt, int64_t ld, int64_t n, int d_pad,
   cuuint64_t gstride[1] = {(cuuint64_t)(ld * vb)};
   cuuint32_t box[2] = {(cuuint32_t)kP, (cuuint32_t)bk};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(&map,
-                   f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64
-                       : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+  const CUtensorMapDataType tdt =
+      f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64
+          : (!vs ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                 : (dtype == EXEM_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                       : CU_TENSOR_MAP_DATA_TYPE_FLOAT16));
+  CUresult r = enc(&map, tdt,
                    2, const_cast<void *>(vt), gdim, gstride, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                    getenv("EXEM_K2_L2P0") ? CU_TENSOR_MAP_L2_PROMOTION_NONE
@@ -463,11 +531,22 @@ int set_min_tma(int dtype, const void *vt, int64_t ld, int64_t n, int d_pad,
   const int64_t tiles = ceil_div(n, kP);
   const int sms = sm_count();
   cudaError_t e = cudaErrorInvalidValue;
-#define EXEM_SMT(DTV, EGV, ETV)                                              \
-  if (eg == EGV && et == ETV)                                                \
-  e = launch_t<DTV, EGV, ETV>(map, tiles, sms, st, n, d_pad, norms, aux,    \
-                              elems, enorms, k, include_aux, t_out,         \
-                              label_out, partials, dist_out, ldd)
+#define EXEM_SMTV(DTV, EGV, ETV, VSV)                                        \
+  if (eg == EGV && et == ETV && vs == VSV)                                   \
+  e = launch_t<DTV, EGV, ETV, VSV>(map, tiles, sms, st, n, d_pad, norms,    \
+                                   aux, elems, enorms, k, include_aux,      \
+                                   t_out, label_out, partials, dist_out,    \
+                                   ldd)
+#define EXEM_SMT(DTV, EGV, ETV) EXEM_SMTV(DTV, EGV, ETV, false)
+#define EXEM_SMT_HALF(DTV, EGV) EXEM_SMTV(DTV, EGV, 8, false)
+#define EXEM_SMTS_WIDE(DTV, EGV)                                             \
+  EXEM_SMTV(DTV, EGV, 5, true); EXEM_SMTV(DTV, EGV, 6, true);               \
+  EXEM_SMTV(DTV, EGV, 7, true); EXEM_SMTV(DTV, EGV, 8, true)
+#define EXEM_SMTS_ONE(DTV)                                                   \
+  EXEM_SMTV(DTV, 1, 1, true); EXEM_SMTV(DTV, 1, 2, true);                   \
+  EXEM_SMTV(DTV, 1, 3, true); EXEM_SMTV(DTV, 1, 4, true);                   \
+  EXEM_SMTV(DTV, 1, 5, true); EXEM_SMTV(DTV, 1, 6, true);                   \
+  EXEM_SMTV(DTV, 1, 7, true); EXEM_SMTV(DTV, 1, 8, true)
 #define EXEM_SMT_WIDE(DTV, EGV)                                              \
   EXEM_SMT(DTV, EGV, 5); EXEM_SMT(DTV, EGV, 6); EXEM_SMT(DTV, EGV, 7);      \
   EXEM_SMT(DTV, EGV, 8)
@@ -488,16 +567,26 @@ int set_min_tma(int dtype, const void *vt, int64_t ld, int64_t n, int d_pad,
       EXEM_SMT_WIDE(EXEM_F32, 8);
       break;
     case EXEM_F16:
-      EXEM_SMT(EXEM_F16, 1, 8); EXEM_SMT(EXEM_F16, 2, 8);
-      EXEM_SMT(EXEM_F16, 4, 8); EXEM_SMT(EXEM_F16, 8, 8);
+      EXEM_SMT_HALF(EXEM_F16, 1); EXEM_SMT_HALF(EXEM_F16, 2);
+      EXEM_SMT_HALF(EXEM_F16, 4); EXEM_SMT_HALF(EXEM_F16, 8);
+      EXEM_SMTS_ONE(EXEM_F16);
+      EXEM_SMTS_WIDE(EXEM_F16, 2); EXEM_SMTS_WIDE(EXEM_F16, 4);
+      EXEM_SMTS_WIDE(EXEM_F16, 8);
       break;
     case EXEM_BF16:
-      EXEM_SMT(EXEM_BF16, 1, 8); EXEM_SMT(EXEM_BF16, 2, 8);
-      EXEM_SMT(EXEM_BF16, 4, 8); EXEM_SMT(EXEM_BF16, 8, 8);
+      EXEM_SMT_HALF(EXEM_BF16, 1); EXEM_SMT_HALF(EXEM_BF16, 2);
+      EXEM_SMT_HALF(EXEM_BF16, 4); EXEM_SMT_HALF(EXEM_BF16, 8);
+      EXEM_SMTS_ONE(EXEM_BF16);
+      EXEM_SMTS_WIDE(EXEM_BF16, 2); EXEM_SMTS_WIDE(EXEM_BF16, 4);
+      EXEM_SMTS_WIDE(EXEM_BF16, 8);
       break;
     default:
       return 1;
   }
+#undef EXEM_SMT_HALF
+#undef EXEM_SMTS_WIDE
+#undef EXEM_SMTS_ONE
+#undef EXEM_SMTV
 #undef EXEM_SMT_ONE
 #undef EXEM_SMT_WIDE
 #undef EXEM_SMT

@@ -75,24 +75,26 @@ __device__ __forceinline__ double nonfinite_mark(bool mark, double nrm,
   return term;
 }
 
-template <int DT>
+template <int DT, bool VS>
 __global__ void __launch_bounds__(kRedThreads)
     ground_prepare_kernel(const typename Traits<DT>::S *__restrict__ src,
                           int64_t n, int d, int d_pad,
                           const typename Traits<DT>::S *__restrict__ e0,
-                          typename Traits<DT>::C *__restrict__ vt, int64_t ld,
+                          typename VtOf<DT, VS>::T *__restrict__ vt, int64_t ld,
                           double *__restrict__ norms,
                           typename Traits<DT>::C *__restrict__ aux,
                           double *__restrict__ partials, bool mark) {
   using S = typename Traits<DT>::S;
   using C = typename Traits<DT>::C;
+  using V = typename VtOf<DT, VS>::T;
   __shared__ double sh[32];
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   double nrm = 0.0, dst = 0.0;
   if (i < ld) {
     // HBM-bound: kLoadAheadK1 independent coalesced loads in flight per
     // thread, then the stores and the (same-order) fp64 accumulations
-    constexpr int kLoadAheadK1 = 8;
+    // (16 for 2-byte sources: the same bytes in flight)
+    constexpr int kLoadAheadK1 = sizeof(S) == 2 ? 16 : 8;
     const bool live = i < n;
     int k = 0;
     for (; k + kLoadAheadK1 <= d; k += kLoadAheadK1) {
@@ -102,7 +104,7 @@ __global__ void __launch_bounds__(kRedThreads)
         xs[u] = live ? to_c(src[(int64_t)(k + u) * n + i]) : C(0);
 #pragma unroll
       for (int u = 0; u < kLoadAheadK1; ++u) {
-        vt[(int64_t)(k + u) * ld + i] = xs[u];
+        vt[(int64_t)(k + u) * ld + i] = to_vt<V>(xs[u]);
         if (live) {
           double xd = (double)xs[u];
           nrm += xd * xd;
@@ -114,7 +116,7 @@ __global__ void __launch_bounds__(kRedThreads)
     for (; k < d_pad; ++k) {
       C x = C(0);
       if (k < d && live) x = to_c(src[(int64_t)k * n + i]);
-      vt[(int64_t)k * ld + i] = x;
+      vt[(int64_t)k * ld + i] = to_vt<V>(x);
       if (k < d && live) {
         double xd = (double)x;
         nrm += xd * xd;
@@ -145,17 +147,18 @@ __global__ void __launch_bounds__(kRedThreads)
 // reads with a 33-element row pitch), then exactly the per-point arithmetic
 // and block partials of ground_prepare_kernel -- results are bit-identical
 // to the column-major path.
-template <int DT>
+template <int DT, bool VS>
 __global__ void __launch_bounds__(kRedThreads)
     ground_prepare_rows_kernel(const typename Traits<DT>::S *__restrict__ src,
                                int64_t n, int d, int d_pad,
                                const typename Traits<DT>::S *__restrict__ e0,
-                               typename Traits<DT>::C *__restrict__ vt,
+                               typename VtOf<DT, VS>::T *__restrict__ vt,
                                int64_t ld, double *__restrict__ norms,
                                typename Traits<DT>::C *__restrict__ aux,
                                double *__restrict__ partials, bool mark) {
   using S = typename Traits<DT>::S;
   using C = typename Traits<DT>::C;
+  using V = typename VtOf<DT, VS>::T;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C(*tile)[33] = reinterpret_cast<C(*)[33]>(smem_raw);  // [256][33]
   __shared__ double sh[32];
@@ -185,7 +188,7 @@ __global__ void __launch_bounds__(kRedThreads)
       for (int kk = 0; kk < 32 && k0 + kk < d_pad; ++kk) {
         const int k = k0 + kk;
         const C x = tile[threadIdx.x][kk];
-        vt[(int64_t)k * ld + i] = x;
+        vt[(int64_t)k * ld + i] = to_vt<V>(x);
         if (k < d && i < n) {
           double xd = (double)x;
           nrm += xd * xd;
@@ -228,6 +231,7 @@ int set_min_tma(int dtype, const void *vt, int64_t ld, int64_t n, int d_pad,
                 const double *enorms, int k, int include_aux, void *t_out,
                 int64_t *label_out, double *partials, void *dist_out,
                 int64_t ldd, cudaStream_t st);
+int set_min_storage_ok(int dtype, int64_t d, int64_t k, int has_t_out);
 
 // ============================================================ K2 set_min
 // min_distances / _set_value / assign_clusters over ONE explicit set
@@ -540,12 +544,12 @@ __global__ void __launch_bounds__(kRedThreads)
 // ============================================================ K2 greedy update
 // m_i <- min(m_i, d(v_i, c*)), c* read from sel_idx[step] on device.
 // Optionally refreshes the TC point operand's folded -h columns.
-template <int DT>
+template <int DT, bool VS>
 __global__ void __launch_bounds__(kRedThreads)
-    greedy_update_kernel(const typename Traits<DT>::C *__restrict__ vt,
+    greedy_update_kernel(const typename VtOf<DT, VS>::T *__restrict__ vt,
                          int64_t ld, int64_t n, int d,
                          const double *__restrict__ norms,
-                         const typename Traits<DT>::C *__restrict__ cvt,
+                         const typename VtOf<DT, VS>::T *__restrict__ cvt,
                          int64_t ldc, const double *__restrict__ cnorms,
                          const int64_t *__restrict__ sel_idx, int64_t step,
                          typename Traits<DT>::C *__restrict__ m,
@@ -562,14 +566,16 @@ __global__ void __launch_bounds__(kRedThreads)
   } else if (i < n) {
     C acc = C(0);
     int kk = 0;
-    for (; kk + kLoadAhead <= d; kk += kLoadAhead) {  // loads ahead (MLP)
-      C xs[kLoadAhead];
+    // loads ahead (MLP; 16 of 2-byte storage: the same bytes in flight)
+    constexpr int LA = VS ? 2 * kLoadAhead : kLoadAhead;
+    for (; kk + LA <= d; kk += LA) {
+      C xs[LA];
 #pragma unroll
-      for (int u = 0; u < kLoadAhead; ++u)
-        xs[u] = vt[(int64_t)(kk + u) * ld + i];
+      for (int u = 0; u < LA; ++u)
+        xs[u] = to_c(vt[(int64_t)(kk + u) * ld + i]);
 #pragma unroll
-      for (int u = 0; u < kLoadAhead; ++u) {
-        const C y = cvt[(int64_t)(kk + u) * ldc + c];
+      for (int u = 0; u < LA; ++u) {
+        const C y = to_c(cvt[(int64_t)(kk + u) * ldc + c]);
         if (Traits<DT>::kDirect) {
           const C df = xs[u] - y;
           acc = fma(df, df, acc);
@@ -579,8 +585,8 @@ __global__ void __launch_bounds__(kRedThreads)
       }
     }
     for (; kk < d; ++kk) {
-      const C x = vt[(int64_t)kk * ld + i];
-      const C y = cvt[(int64_t)kk * ldc + c];
+      const C x = to_c(vt[(int64_t)kk * ld + i]);
+      const C y = to_c(cvt[(int64_t)kk * ldc + c]);
       if (Traits<DT>::kDirect) {
         const C df = x - y;
         acc = fma(df, df, acc);
@@ -1234,7 +1240,7 @@ using namespace exem;
 extern "C" {
 
 const char *exem_last_error(void) { return g_err; }
-int exem_abi_version(void) { return 3; }
+int exem_abi_version(void) { return 4; }
 int64_t exem_launch_count(void) {
   return (int64_t)__atomic_load_n(&g_launches, __ATOMIC_RELAXED);
 }
@@ -1285,11 +1291,12 @@ int exem_ground_prepare(int dtype, const void *src, int64_t n, int64_t d,
   cudaStream_t st = (cudaStream_t)stream;
   const int d_pad = (int)exem_pad_dims(d);
   const int64_t blocks = ceil_div(ld, kRedThreads);
-  EXEM_DISPATCH(dtype, DT, {
+  EXEM_DISPATCH_VT(dtype, DT, VS, {
     using S = typename Traits<DT>::S;
     using C = typename Traits<DT>::C;
-    ground_prepare_kernel<DT><<<(unsigned)blocks, kRedThreads, 0, st>>>(
-        (const S *)src, n, (int)d, d_pad, (const S *)e0, (C *)vt, ld, norms,
+    using V = typename VtOf<DT, VS>::T;
+    ground_prepare_kernel<DT, VS><<<(unsigned)blocks, kRedThreads, 0, st>>>(
+        (const S *)src, n, (int)d, d_pad, (const S *)e0, (V *)vt, ld, norms,
         (C *)aux, scratch, check_finite != 0);
     EXEM_LAUNCH_CHECK("ground_prepare_kernel");
   });
@@ -1345,6 +1352,10 @@ int exem_h2d_rows(void *dst, const void *host, int64_t ld_host, int64_t row0,
   return EXEM_OK;
 }
 
+int exem_set_min_storage_ok(int dtype, int64_t d, int64_t k, int has_t_out) {
+  return set_min_storage_ok(dtype, d, k, has_t_out);
+}
+
 int exem_set_min(int dtype, const void *vt, int64_t ld, int64_t n, int64_t d,
                  const double *norms, const void *aux, const void *elems,
                  const double *enorms, int64_t k, int include_aux, void *t_out,
@@ -1355,6 +1366,23 @@ int exem_set_min(int dtype, const void *vt, int64_t ld, int64_t n, int64_t d,
   cudaStream_t st = (cudaStream_t)stream;
   const int d_pad = (int)exem_pad_dims(d);
   const int64_t blocks = ceil_div(n, kRedThreads);
+  if (dtype & EXEM_VT_STORAGE) {
+    // 2-byte storage-typed vt: the TMA-fed K2 only (it widens in registers)
+    if (!set_min_storage_ok(dtype, d, k, t_out != nullptr) || ld % kSmP)
+      return fail(EXEM_ERR_ARG,
+                  "set_min: storage-typed vt is not covered for d=%lld k=%lld "
+                  "(exem_set_min_storage_ok)", (long long)d, (long long)k);
+    const int tma = set_min_tma(dtype, vt, ld, n, d_pad, norms, aux, elems,
+                                enorms, (int)k, include_aux, t_out, label_out,
+                                scratch, nullptr, 0, st);
+    if (tma != 0)
+      return fail(tma > 0 ? EXEM_ERR_ARG : EXEM_ERR_CUDA, "set_min (TMA): %s",
+                  tma > 0 ? "shape not covered"
+                          : cudaGetErrorString((cudaError_t)(-tma)));
+    count_launch();
+    if (sum_out) return reduce_fixed(scratch, blocks, sum_out, 0, st);
+    return EXEM_OK;
+  }
   EXEM_DISPATCH(dtype, DT, {
     using C = typename Traits<DT>::C;
     cudaError_t e = launch_set_min<DT>(
@@ -1392,11 +1420,12 @@ int exem_greedy_update(int dtype, const void *vt, int64_t ld, int64_t n,
                        void *stream) {
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t blocks = ceil_div(n, kRedThreads);
-  EXEM_DISPATCH(dtype, DT, {
+  EXEM_DISPATCH_VT(dtype, DT, VS, {
     using S = typename Traits<DT>::S;
     using C = typename Traits<DT>::C;
-    greedy_update_kernel<DT><<<(unsigned)blocks, kRedThreads, 0, st>>>(
-        (const C *)vt, ld, n, (int)d, norms, (const C *)cvt, ldc, cnorms,
+    using V = typename VtOf<DT, VS>::T;
+    greedy_update_kernel<DT, VS><<<(unsigned)blocks, kRedThreads, 0, st>>>(
+        (const V *)vt, ld, n, (int)d, norms, (const V *)cvt, ldc, cnorms,
         sel_idx, step, (C *)m, (S *)xp, kp, scratch);
     EXEM_LAUNCH_CHECK("greedy_update_kernel");
   });
@@ -1810,20 +1839,21 @@ int exem_ground_prepare_rows(int dtype, const void *src, int64_t n, int64_t d,
   cudaStream_t st = (cudaStream_t)stream;
   const int d_pad = (int)exem_pad_dims(d);
   const int64_t blocks = ceil_div(ld, kRedThreads);
-  EXEM_DISPATCH(dtype, DT, {
+  EXEM_DISPATCH_VT(dtype, DT, VS, {
     using S = typename Traits<DT>::S;
     using C = typename Traits<DT>::C;
+    using V = typename VtOf<DT, VS>::T;
     const size_t smem = (size_t)kRedThreads * 33 * sizeof(C);
     if (smem > 48 * 1024) {
       cudaError_t e = cudaFuncSetAttribute(
-          ground_prepare_rows_kernel<DT>,
+          ground_prepare_rows_kernel<DT, VS>,
           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess)
         return fail(EXEM_ERR_CUDA, "prepare_rows smem: %s",
                     cudaGetErrorString(e));
     }
-    ground_prepare_rows_kernel<DT><<<(unsigned)blocks, kRedThreads, smem, st>>>(
-        (const S *)src, n, (int)d, d_pad, (const S *)e0, (C *)vt, ld, norms,
+    ground_prepare_rows_kernel<DT, VS><<<(unsigned)blocks, kRedThreads, smem, st>>>(
+        (const S *)src, n, (int)d, d_pad, (const S *)e0, (V *)vt, ld, norms,
         (C *)aux, scratch, check_finite != 0);
     EXEM_LAUNCH_CHECK("ground_prepare_rows_kernel");
   });

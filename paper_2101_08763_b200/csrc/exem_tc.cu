@@ -723,8 +723,9 @@ __global__ void __launch_bounds__(Epi<kQ, kBN>::kThreads, 1)
 // ---------------------------------------------------------------- packing
 // Transposes the SIMT layout vt[d_pad][ld] into point-major half rows and
 // appends the folded constant columns (see header comment).
-template <int DT, bool kCand>
-__global__ void pack_kernel(const float *__restrict__ vt, int64_t ld,
+template <int DT, bool kCand, bool VS>
+__global__ void pack_kernel(const typename VtOf<DT, VS>::T *__restrict__ vt,
+                            int64_t ld,
                             int64_t n, int d, const double *__restrict__ norms,
                             const float *__restrict__ m,
                             typename Traits<DT>::S *__restrict__ x, int64_t kp,
@@ -737,7 +738,7 @@ __global__ void pack_kernel(const float *__restrict__ vt, int64_t ld,
   for (int ty = threadIdx.y; ty < 32; ty += blockDim.y) {
     const int k = k0 + ty;
     const int64_t r = r0 + threadIdx.x;
-    tile[ty][threadIdx.x] = (k < d && r < n) ? vt[(int64_t)k * ld + r] : 0.f;
+    tile[ty][threadIdx.x] = (k < d && r < n) ? to_c(vt[(int64_t)k * ld + r]) : 0.f;
   }
   __syncthreads();
   for (int ty = threadIdx.y; ty < 32; ty += blockDim.y) {
@@ -856,20 +857,24 @@ extern "C" {
 int exem_tc_pack_candidates(int dtype, const void *vt, int64_t ld, int64_t n,
                             int64_t d, const double *norms, void *xc,
                             void *stream) {
-  if (dtype != EXEM_BF16 && dtype != EXEM_F16)
+  const int tag = dtype & ~EXEM_VT_STORAGE;
+  if (tag != EXEM_BF16 && tag != EXEM_F16)
     return fail(EXEM_ERR_ARG, "TC operands are bf16/f16 only");
   const int64_t kp = exem_tc_kp(d), rows = exem_tc_rows(n);
   dim3 grid((unsigned)ceil_div(rows, 32), (unsigned)ceil_div(kp, 32));
   dim3 block(32, 8);
   cudaStream_t st = (cudaStream_t)stream;
-  if (dtype == EXEM_BF16)
-    tc::pack_kernel<EXEM_BF16, true><<<grid, block, 0, st>>>(
-        (const float *)vt, ld, n, (int)d, norms, nullptr,
-        (__nv_bfloat16 *)xc, kp, rows);
-  else
-    tc::pack_kernel<EXEM_F16, true><<<grid, block, 0, st>>>(
-        (const float *)vt, ld, n, (int)d, norms, nullptr, (__half *)xc, kp,
-        rows);
+  const bool vs = (dtype & EXEM_VT_STORAGE) != 0;
+#define EXEM_PACK(DT, VS)                                                    \
+  tc::pack_kernel<DT, true, VS><<<grid, block, 0, st>>>(                     \
+      (const typename VtOf<DT, VS>::T *)vt, ld, n, (int)d, norms, nullptr,   \
+      (typename Traits<DT>::S *)xc, kp, rows)
+  if (tag == EXEM_BF16) {
+    if (vs) EXEM_PACK(EXEM_BF16, true); else EXEM_PACK(EXEM_BF16, false);
+  } else {
+    if (vs) EXEM_PACK(EXEM_F16, true); else EXEM_PACK(EXEM_F16, false);
+  }
+#undef EXEM_PACK
   EXEM_LAUNCH_CHECK("tc_pack_candidates");
   return EXEM_OK;
 }
@@ -877,20 +882,24 @@ int exem_tc_pack_candidates(int dtype, const void *vt, int64_t ld, int64_t n,
 int exem_tc_pack_points(int dtype, const void *vt, int64_t ld, int64_t n,
                         int64_t d, const double *norms, const void *m,
                         void *xp, void *stream) {
-  if (dtype != EXEM_BF16 && dtype != EXEM_F16)
+  const int tag = dtype & ~EXEM_VT_STORAGE;
+  if (tag != EXEM_BF16 && tag != EXEM_F16)
     return fail(EXEM_ERR_ARG, "TC operands are bf16/f16 only");
   const int64_t kp = exem_tc_kp(d), rows = exem_tc_rows(n);
   dim3 grid((unsigned)ceil_div(rows, 32), (unsigned)ceil_div(kp, 32));
   dim3 block(32, 8);
   cudaStream_t st = (cudaStream_t)stream;
-  if (dtype == EXEM_BF16)
-    tc::pack_kernel<EXEM_BF16, false><<<grid, block, 0, st>>>(
-        (const float *)vt, ld, n, (int)d, norms, (const float *)m,
-        (__nv_bfloat16 *)xp, kp, rows);
-  else
-    tc::pack_kernel<EXEM_F16, false><<<grid, block, 0, st>>>(
-        (const float *)vt, ld, n, (int)d, norms, (const float *)m,
-        (__half *)xp, kp, rows);
+  const bool vs = (dtype & EXEM_VT_STORAGE) != 0;
+#define EXEM_PACK(DT, VS)                                                    \
+  tc::pack_kernel<DT, false, VS><<<grid, block, 0, st>>>(                    \
+      (const typename VtOf<DT, VS>::T *)vt, ld, n, (int)d, norms,            \
+      (const float *)m, (typename Traits<DT>::S *)xp, kp, rows)
+  if (tag == EXEM_BF16) {
+    if (vs) EXEM_PACK(EXEM_BF16, true); else EXEM_PACK(EXEM_BF16, false);
+  } else {
+    if (vs) EXEM_PACK(EXEM_F16, true); else EXEM_PACK(EXEM_F16, false);
+  }
+#undef EXEM_PACK
   EXEM_LAUNCH_CHECK("tc_pack_points");
   return EXEM_OK;
 }

@@ -750,8 +750,9 @@ __global__ void pack_sets_kernel(const float *__restrict__ packed,
 }
 
 // Plain point rows [v, 0..] (kp = round_up(d, 64)) for unfolded K4-TC.
-template <int DT>
-__global__ void pack_plain_kernel(const float *__restrict__ vt, int64_t ld,
+template <int DT, bool VS>
+__global__ void pack_plain_kernel(const typename VtOf<DT, VS>::T *__restrict__ vt,
+                                  int64_t ld,
                                   int64_t n, int d,
                                   typename Traits<DT>::S *__restrict__ x,
                                   int64_t kp, int64_t rows) {
@@ -762,7 +763,7 @@ __global__ void pack_plain_kernel(const float *__restrict__ vt, int64_t ld,
   for (int ty = threadIdx.y; ty < 32; ty += blockDim.y) {
     const int k = k0 + ty;
     const int64_t r = r0 + threadIdx.x;
-    tile[ty][threadIdx.x] = (k < d && r < n) ? vt[(int64_t)k * ld + r] : 0.f;
+    tile[ty][threadIdx.x] = (k < d && r < n) ? to_c(vt[(int64_t)k * ld + r]) : 0.f;
   }
   __syncthreads();
   for (int ty = threadIdx.y; ty < 32; ty += blockDim.y) {
@@ -861,18 +862,24 @@ int64_t exem_tc_batch_kp(int64_t d) {
 
 int exem_tc_pack_points_plain(int dtype, const void *vt, int64_t ld,
                               int64_t n, int64_t d, void *xp, void *stream) {
-  if (dtype != EXEM_BF16 && dtype != EXEM_F16)
+  const int tag = dtype & ~EXEM_VT_STORAGE;
+  if (tag != EXEM_BF16 && tag != EXEM_F16)
     return fail(EXEM_ERR_ARG, "TC operands are bf16/f16 only");
   const int64_t kp = round_up(d, kTcKChunk), rows = exem_tc_rows(n);
   dim3 grid((unsigned)ceil_div(rows, 32), (unsigned)ceil_div(kp, 32));
   dim3 block(32, 8);
   cudaStream_t st = (cudaStream_t)stream;
-  if (dtype == EXEM_BF16)
-    tcb::pack_plain_kernel<EXEM_BF16><<<grid, block, 0, st>>>(
-        (const float *)vt, ld, n, (int)d, (__nv_bfloat16 *)xp, kp, rows);
-  else
-    tcb::pack_plain_kernel<EXEM_F16><<<grid, block, 0, st>>>(
-        (const float *)vt, ld, n, (int)d, (__half *)xp, kp, rows);
+  const bool vs = (dtype & EXEM_VT_STORAGE) != 0;
+#define EXEM_PACK(DT, VS)                                                    \
+  tcb::pack_plain_kernel<DT, VS><<<grid, block, 0, st>>>(                    \
+      (const typename VtOf<DT, VS>::T *)vt, ld, n, (int)d,                   \
+      (typename Traits<DT>::S *)xp, kp, rows)
+  if (tag == EXEM_BF16) {
+    if (vs) EXEM_PACK(EXEM_BF16, true); else EXEM_PACK(EXEM_BF16, false);
+  } else {
+    if (vs) EXEM_PACK(EXEM_F16, true); else EXEM_PACK(EXEM_F16, false);
+  }
+#undef EXEM_PACK
   EXEM_LAUNCH_CHECK("tc_pack_points_plain");
   return EXEM_OK;
 }

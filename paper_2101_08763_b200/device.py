@@ -128,7 +128,18 @@ class DeviceGround:
         self.split_pts = int(lib.split_points(self.n))
         self.splits = int(lib.num_splits(self.n))
         cdt = compute_torch_dtype(precision)
-        self.vt = t.empty((self.d_pad, self.ld), dtype=cdt, device=self.dev)
+        self.cdtype = cdt
+        # bf16/f16 ground sets keep V at its 2-byte storage type
+        # (EXEM_VT_STORAGE): K1 writes it, K2 / the m-update / the TC
+        # operand packers read it; the binary32 widening is materialised
+        # only for the CUDA-core consumers that need it (vt_c)
+        self.vt_flag = N.VT_STORAGE if precision.is_half else 0
+        if self.vt_flag:
+            vdt = t.bfloat16 if precision.tag == N.BF16 else t.float16
+        else:
+            vdt = cdt
+        self.vt = t.empty((self.d_pad, self.ld), dtype=vdt, device=self.dev)
+        self._vt_c = None
         self.norms = t.empty(self.ld, dtype=t.float64, device=self.dev)
         self.aux = t.empty(self.ld, dtype=cdt, device=self.dev)
         self.scratch = t.empty(int(lib.reduce_scratch(self.ld)),
@@ -139,19 +150,44 @@ class DeviceGround:
         self.kp = int(lib.tc_kp(self.d)) if precision.is_half else 0
         self._max_norm = None
 
+    @property
+    def vt_tag(self) -> int:
+        """dtype tag of the entry points that read/write ``vt``."""
+        return self.precision.tag | self.vt_flag
+
+    def vt_c(self):
+        """``vt`` at the compute type: ``vt`` itself for f32/f64; for half
+        ground sets a binary32 widening built on first use (exem_widen_packed
+        over the whole [d_pad][ld] buffer) for the CUDA-core kernels that
+        read 4-byte V (K3-SIMT, K4, the sieve's distance rows, K2 shapes the
+        TMA kernel does not cover)."""
+        if not self.vt_flag:
+            return self.vt
+        if self._vt_c is None:
+            t = torch()
+            lib = N.lib()
+            with t.cuda.device(self.device_index):
+                out = t.empty((self.d_pad, self.ld), dtype=self.cdtype,
+                              device=self.dev)
+                lib.widen_packed(self.precision.tag, N.ptr(self.vt), self.ld,
+                                 self.ld, 1, self.d_pad, N.ptr(out),
+                                 self.stream)
+            self._vt_c = out
+        return self._vt_c
+
     def column_major_storage(self) -> np.ndarray:
         """(n, d) column-major host array of the STORED values (the
         reference's GroundSet.matrix layout), read back from ``vt``: exact,
-        since vt holds the storage values widened to the compute type."""
+        since vt holds the storage values (or, at f32/f64, the values)."""
         t = torch()
         tag = self.precision.tag
         with t.cuda.device(self.device_index):
             v = self.vt[: self.d, : self.n]
             if tag == N.BF16:
-                host = v.to(t.bfloat16).view(t.int16).cpu().numpy().view(
+                host = v.contiguous().view(t.int16).cpu().numpy().view(
                     self.precision.dtype)
             elif tag == N.F16:
-                host = v.to(t.float16).cpu().numpy()
+                host = v.contiguous().cpu().numpy()
             else:
                 host = v.contiguous().cpu().numpy()
         return host.T  # (d, n) C-order == (n, d) F-order
@@ -177,7 +213,7 @@ class DeviceGround:
             rows = int(lib.tc_rows(self.n))
             tdt = t.bfloat16 if self.precision.tag == N.BF16 else t.float16
             self._xp0 = t.empty((rows, self.kp), dtype=tdt, device=self.dev)
-            lib.tc_pack_points(self.precision.tag, N.ptr(self.vt), self.ld,
+            lib.tc_pack_points(self.vt_tag, N.ptr(self.vt), self.ld,
                                self.n, self.d, N.ptr(self.norms), None,
                                N.ptr(self._xp0), self.stream)
         return self._xp0
@@ -194,7 +230,7 @@ class DeviceGround:
             self._xpp = t.empty((int(lib.tc_rows(self.n)),
                                  int(lib.tc_batch_kp(self.d))), dtype=tdt,
                                 device=self.dev)
-            lib.tc_pack_points_plain(self.precision.tag, N.ptr(self.vt),
+            lib.tc_pack_points_plain(self.vt_tag, N.ptr(self.vt),
                                      self.ld, self.n, self.d,
                                      N.ptr(self._xpp), self.stream)
         return self._xpp
@@ -220,7 +256,7 @@ class DeviceGround:
             rows = int(lib.tc_rows(self.n))
             tdt = t.bfloat16 if self.precision.tag == N.BF16 else t.float16
             self._xc = t.empty((rows, self.kp), dtype=tdt, device=self.dev)
-            lib.tc_pack_candidates(self.precision.tag, N.ptr(self.vt), self.ld,
+            lib.tc_pack_candidates(self.vt_tag, N.ptr(self.vt), self.ld,
                                    self.n, self.d, N.ptr(self.norms),
                                    N.ptr(self._xc), self.stream)
         return self._xc
@@ -251,7 +287,7 @@ def prepare_ground(matrix: np.ndarray, aux_vec: np.ndarray, precision,
                       matrix.nbytes, dg.stream)
         prepare = (lib.ground_prepare_rows if row_major(matrix)
                    else lib.ground_prepare)
-        prepare(precision.tag, N.ptr(src), n, d, N.ptr(e0), N.ptr(dg.vt),
+        prepare(dg.vt_tag, N.ptr(src), n, d, N.ptr(e0), N.ptr(dg.vt),
                 dg.ld, N.ptr(dg.norms), N.ptr(dg.aux), N.ptr(dg.aux_sum),
                 N.ptr(dg.scratch), int(check_finite), dg.stream)
         aux_host = dg.aux[:n].cpu().numpy().astype(aux_dtype(precision))

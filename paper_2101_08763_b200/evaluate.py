@@ -227,7 +227,7 @@ def batch_partials(dg, batch: DeviceBatch, partial, split_pts: int,
                           batch.l, batch.k_max, dg.d, split_pts, pp, splits,
                           dg.stream)
     else:
-        lib.batch_eval(prec.tag, N.ptr(dg.vt), dg.ld, dg.n, dg.d,
+        lib.batch_eval(prec.tag, N.ptr(dg.vt_c()), dg.ld, dg.n, dg.d,
                        N.ptr(dg.norms), N.ptr(dg.aux), N.ptr(batch.packed),
                        N.ptr(batch.pnorms), N.ptr(batch.card), batch.l,
                        batch.l_pad, batch.k_max, split_pts, pp, splits,

@@ -186,12 +186,19 @@ def device_set_min(ground: GroundSet, elems: np.ndarray, include_aux: bool,
         # sets larger than one element group of the TMA K2 (64 at 4-byte,
         # 32 at 8-byte compute types) carry the running minimum through
         # t_out: give it one even when only the sum is wanted
-        groups = k > (32 if dg.vt.element_size() == 8 else 64)
-        t_out = (t.empty(dg.n, dtype=dg.vt.dtype, device=dg.dev)
+        groups = k > (32 if dg.cdtype == t.float64 else 64)
+        t_out = (t.empty(dg.n, dtype=dg.cdtype, device=dg.dev)
                  if want_t or groups else None)
         lab = t.empty(dg.n, dtype=t.int64, device=dg.dev) if want_labels else None
         s = t.empty(1, dtype=t.float64, device=dg.dev)
-        lib.set_min(prec.tag, N.ptr(dg.vt), dg.ld, dg.n, dg.d, N.ptr(dg.norms),
+        # 2-byte half storage goes straight to the TMA-fed K2; shapes it
+        # does not cover read the binary32 widening
+        if dg.vt_flag and lib.set_min_storage_ok(dg.vt_tag, dg.d, k,
+                                                 int(t_out is not None)):
+            tag, vt = dg.vt_tag, dg.vt
+        else:
+            tag, vt = prec.tag, dg.vt_c()
+        lib.set_min(tag, N.ptr(vt), dg.ld, dg.n, dg.d, N.ptr(dg.norms),
                     N.ptr(dg.aux), N.ptr(e), N.ptr(en), k, int(include_aux),
                     N.ptr(t_out), N.ptr(lab), N.ptr(s), N.ptr(dg.scratch), st)
         total = float(s.item())

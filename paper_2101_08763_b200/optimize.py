@@ -101,7 +101,7 @@ class GreedyRun:
         self.splits = -(-dg.n // self.split_pts)
         self.l = self.cand.n
         dev = dg.dev
-        self.m = t.empty(dg.ld, dtype=dg.vt.dtype, device=dev)
+        self.m = t.empty(dg.ld, dtype=dg.cdtype, device=dev)
         self.selected = t.zeros(max(self.l, 1), dtype=t.uint8, device=dev)
         self.gains = t.empty(self.l, dtype=t.float64, device=dev)
         self.sel_idx = t.zeros(k_cap, dtype=t.int64, device=dev)
@@ -154,7 +154,7 @@ class GreedyRun:
                               N.ptr(dg.norms), N.ptr(self.m), N.ptr(self.xp),
                               self.stream)
         elif self.tc:
-            lib.tc_pack_points(self.prec.tag, N.ptr(dg.vt), dg.ld, dg.n, dg.d,
+            lib.tc_pack_points(dg.vt_tag, N.ptr(dg.vt), dg.ld, dg.n, dg.d,
                                N.ptr(dg.norms), N.ptr(self.m), N.ptr(self.xp),
                                self.stream)
 
@@ -163,7 +163,7 @@ class GreedyRun:
         ``self.gains`` or the device buffer at pointer ``out``."""
         dg, cd, lib, st = self.dg, self.cand, self.lib, self.stream
         chunk = self.l if not chunk or chunk >= self.l else chunk
-        esz = dg.vt.element_size()
+        esz = dg.vt_c().element_size() if not self.tc else 0
         for c0 in range(0, self.l, chunk):
             cl = min(chunk, self.l - c0)
             part = self.partial(cl)
@@ -177,10 +177,12 @@ class GreedyRun:
                                        2 if probe else self.epi,
                                        N.ptr(self.hits) if probe else None, st)
             else:
-                cvt_ptr = N.c_void_p(cd.vt.data_ptr() + c0 * esz)
+                # the CUDA-core K3 reads 4/8-byte V (widened half storage)
+                cvt_ptr = N.c_void_p(cd.vt_c().data_ptr() + c0 * esz)
                 cn_ptr = N.c_void_p(cd.norms.data_ptr() + c0 * 8)
                 lib.greedy_gains_simt(self.prec.tag, cvt_ptr, cd.ld, cn_ptr,
-                                      cl, N.ptr(dg.vt), dg.ld, N.ptr(dg.norms),
+                                      cl, N.ptr(dg.vt_c()), dg.ld,
+                                      N.ptr(dg.norms),
                                       N.ptr(self.m), dg.n, dg.d,
                                       self.split_pts, N.ptr(part),
                                       self.splits, st)
@@ -210,8 +212,9 @@ class GreedyRun:
     def update(self, step: int):
         """K2: m_i <- min(m_i, d(v_i, c*)); msum[step] = sum_i m_i."""
         dg, cd = self.dg, self.cand
+        assert dg.vt_flag == cd.vt_flag  # same precision: same vt layout
         self.lib.greedy_update(
-            self.prec.tag, N.ptr(dg.vt), dg.ld, dg.n, dg.d, N.ptr(dg.norms),
+            dg.vt_tag, N.ptr(dg.vt), dg.ld, dg.n, dg.d, N.ptr(dg.norms),
             N.ptr(cd.vt), cd.ld, N.ptr(cd.norms), N.ptr(self.sel_idx), step,
             N.ptr(self.m), None if self.split32 else N.ptr(self.xp), dg.kp,
             N.ptr(self.msum), N.ptr(self.scratch), self.stream)

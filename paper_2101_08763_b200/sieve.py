@@ -124,7 +124,7 @@ def sieve_streaming_maximize(ground: GroundSet, k: int, eps: float = 0.1,
             nb = len(idx)
             E = padded_rows(ground.matrix[idx], dg.d_pad, prec, dg.dev)
             lib.row_norms(prec.tag, N.ptr(E), nb, dg.d, dg.d_pad, N.ptr(en), st)
-            lib.sieve_block_dist(prec.tag, N.ptr(dg.vt), dg.ld, n, dg.d,
+            lib.sieve_block_dist(prec.tag, N.ptr(dg.vt_c()), dg.ld, n, dg.d,
                                  N.ptr(dg.norms), N.ptr(E), N.ptr(en), nb,
                                  N.ptr(D), dg.ld, N.ptr(scratch), st)
             lib.sieve_block_gains(prec.tag, N.ptr(M), dg.ld, rows, N.ptr(D),

@@ -162,6 +162,17 @@ class _Slot:
     def vt(self):
         return self._vt[: self.d_pad * self.ld].view(self.d_pad, self.ld)
 
+    # a slot's vt is always at the compute type (the streamed path keeps
+    # the widened layout; DeviceGround keeps half storage at 2 bytes)
+    vt_flag = 0
+
+    def vt_c(self):
+        return self.vt
+
+    @property
+    def vt_tag(self) -> int:
+        return self.precision.tag
+
     @property
     def stream(self):
         return N.stream_handle(self.dev)

@@ -58,10 +58,35 @@ def test_binding_covers_header(native_lib):
     assert sorted(_native.EXPORTED) == _header_symbols()
 
 
+def test_header_constants_match_binding():
+    from paper_2101_08763_b200 import _native
+
+    text = (ROOT / "include" / "exem_b200.h").read_text()
+    consts = dict(re.findall(r"#define (EXEM_[A-Z0-9_]+) (0x[0-9a-fA-F]+|\d+)",
+                             text))
+    val = {k: int(v, 0) for k, v in consts.items()}
+    assert val["EXEM_VT_STORAGE"] == _native.VT_STORAGE
+    assert (val["EXEM_F16"], val["EXEM_BF16"], val["EXEM_F32"],
+            val["EXEM_F64"]) == (_native.F16, _native.BF16, _native.F32,
+                                 _native.F64)
+    # the flag never collides with a tag
+    assert all(t & _native.VT_STORAGE == 0 for t in range(4))
+
+
+def test_storage_ok_predicate(native_lib):
+    """exem_set_min_storage_ok is pure host arithmetic (no device work)."""
+    from paper_2101_08763_b200 import _native as N
+
+    ok = native_lib.set_min_storage_ok
+    assert ok(N.F32 | N.VT_STORAGE, 100, 10, 0) == 0
+    assert ok(N.F32, 100, 10, 0) == 0
+    assert ok(N.BF16 | N.VT_STORAGE, 100, 0, 0) == 0
+
+
 def test_layout_helpers(native_lib):
     lib = native_lib
     from paper_2101_08763_b200._native import ABI_VERSION
-    assert lib.abi_version() == ABI_VERSION == 3
+    assert lib.abi_version() == ABI_VERSION == 4
     assert lib.pad_points(1) == 256 and lib.pad_points(257) == 512
     assert lib.pad_dims(100) == 104 and lib.pad_dims(2) == 8
     assert lib.tc_kp(100) == 128 and lib.tc_kp(2) == 64 and lib.tc_kp(1024) == 1088

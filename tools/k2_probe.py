@@ -30,7 +30,7 @@ def main():
         en = torch.empty(k, dtype=torch.float64, device=dg.dev)
         lib.row_norms(prec.tag, N.ptr(elems), k, d, dg.d_pad, N.ptr(en), st)
         s = torch.empty(1, dtype=torch.float64, device=dg.dev)
-        lib.set_min(prec.tag, N.ptr(dg.vt), dg.ld, n, d, N.ptr(dg.norms),
+        lib.set_min(dg.vt_tag, N.ptr(dg.vt), dg.ld, n, d, N.ptr(dg.norms),
                     N.ptr(dg.aux), N.ptr(elems), N.ptr(en), k, 1, None, None,
                     N.ptr(s), N.ptr(dg.scratch), st)
     torch.cuda.synchronize()

@@ -33,7 +33,7 @@ def main():
         lib.row_norms(prec.tag, N.ptr(elems), k, d, dg.d_pad, N.ptr(en), st)
         s = torch.empty(1, dtype=torch.float64, device=dg.dev)
         out[k] = round(timed(lambda: lib.set_min(
-            prec.tag, N.ptr(dg.vt), dg.ld, n, d, N.ptr(dg.norms),
+            dg.vt_tag, N.ptr(dg.vt), dg.ld, n, d, N.ptr(dg.norms),
             N.ptr(dg.aux), N.ptr(elems), N.ptr(en), k, 1, None, None,
             N.ptr(s), N.ptr(dg.scratch), st), reps=10) * 1e3, 4)
     print(json.dumps(out))
