@@ -180,6 +180,39 @@ __device__ __forceinline__ double block_sum(double v, double *sh) {
   return r;  // valid in warp 0
 }
 
+// block_sum<256> of 256 point values held two per thread by a 128-thread
+// block (thread t: points 2t, 2t+1), bit for bit: each warp rebuilds the
+// two 32-point warps of block_sum<256> it covers with shuffles, runs the
+// same xor trees, and warp 0 combines the 8 warp sums in the same order.
+__device__ __forceinline__ double pair_block_sum(double v0, double v1,
+                                                 double *sh) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int src_a = lane >> 1, src_b = 16 + (lane >> 1);
+  const double a0 = __shfl_sync(0xffffffffu, v0, src_a);
+  const double a1 = __shfl_sync(0xffffffffu, v1, src_a);
+  const double b0 = __shfl_sync(0xffffffffu, v0, src_b);
+  const double b1 = __shfl_sync(0xffffffffu, v1, src_b);
+  double va = (lane & 1) ? a1 : a0, vb = (lane & 1) ? b1 : b0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    va += __shfl_xor_sync(0xffffffffu, va, o);
+    vb += __shfl_xor_sync(0xffffffffu, vb, o);
+  }
+  if (lane == 0) {
+    sh[2 * w] = va;
+    sh[2 * w + 1] = vb;
+  }
+  __syncthreads();
+  double r = 0.0;
+  if (w == 0) {
+    r = lane < 8 ? sh[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+  }
+  __syncthreads();
+  return r;  // valid in warp 0
+}
+
 // cp.async helpers (16-byte global -> shared)
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);

@@ -47,14 +47,21 @@ constexpr int kStageBytes = 8 * 1024;
 constexpr int kElemSmemMax = 128 * 1024;  // resident element budget
 constexpr int kSmemPerSm = 227 * 1024;
 
-// dimensions per ring stage (8 KB of 4/8-byte V): exactly d_pad =
-// round_up(d, 8) dimensions are streamed (no dead FMAs on padding chunks);
-// 2-byte storage-typed V (EXEM_VT_STORAGE) keeps 8 dimensions in 4 KB stages
-template <typename V> constexpr int bk_of() {
-  return sizeof(V) == 2 ? 8 : kStageBytes / (kP * (int)sizeof(V));
+// dimensions per ring stage (8 KB of V): exactly d_pad = round_up(d, 8)
+// dimensions are streamed (no dead FMAs on padding chunks).  2-byte
+// storage-typed V (EXEM_VT_STORAGE): the HBM-bound layouts (EG <= 2) carry
+// 16 dimensions per 8 KB stage -- when d_pad is an odd multiple of 8 the
+// last box reads 8 rows past d_pad (TMA zero fill, still a full box of
+// transaction bytes) that the kernel skips; 4 KB stages of 8 dimensions ran
+// at the f32 kernel's stage rate (k = 1: 0.090 ms for half the bytes).  The
+// FMA-bound layouts (EG >= 4) keep 8 dimensions in 4 KB stages (16 measured
+// 12-19 % slower at k = 50 / 64).
+template <typename V, int EG> constexpr int bk_of() {
+  return (sizeof(V) == 2 && EG >= 4) ? 8
+                                     : kStageBytes / (kP * (int)sizeof(V));
 }
-template <typename V> constexpr int stage_bytes() {
-  return bk_of<V>() * kP * (int)sizeof(V);
+template <typename V, int EG> constexpr int stage_bytes() {
+  return bk_of<V, EG>() * kP * (int)sizeof(V);
 }
 
 // PT consecutive storage-typed points of one dimension, widened (one
@@ -157,7 +164,7 @@ __global__ void __launch_bounds__(kThreads, min_ctas<EG>())
                        int64_t ldd) {
   using C = typename Traits<DT>::C;
   using VT = typename VtOf<DT, VS>::T;  // element type of the V stages
-  constexpr int BK = bk_of<VT>();
+  constexpr int BK = bk_of<VT, EG>();
   constexpr int PT = EG;              // points per thread
   constexpr int KG = EG * ET;         // elements per group
   constexpr int ROW = EG * 8;         // smem values per dimension
@@ -180,7 +187,7 @@ __global__ void __launch_bounds__(kThreads, min_ctas<EG>())
   const int64_t tiles = (n + kP - 1) / kP;
   const int64_t my_tiles =
       blockIdx.x < tiles ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const int nchunks = d_pad / BK;
+  const int nchunks = (d_pad + BK - 1) / BK;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < nstages; ++s) {
@@ -253,8 +260,7 @@ __global__ void __launch_bounds__(kThreads, min_ctas<EG>())
         tc::mbar_wait_hint(&full[s], (ev_use / nstages) & 1);
         const VT *cv = sv + s * STAGE + pg * PT;
         const C *ce = se + (c * BK) * ROW + eg * 8;
-#pragma unroll(kUnrollKK)
-        for (int kk = 0; kk < BK; ++kk) {
+        auto dim_step = [&](int kk) {
           C pv[PT], ev[8];
           using V4 = typename Vec4<C>::T;
           constexpr int per = 16 / sizeof(C);
@@ -292,6 +298,17 @@ __global__ void __launch_bounds__(kThreads, min_ctas<EG>())
                 acc[p][j] = fma(pv[p], ev[j], acc[p][j]);
               }
             }
+        };
+        if constexpr (BK == 16) {  // 2-byte V: 8 dims, then 8 more unless tail
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) dim_step(kk);
+          if (c * BK + 8 < d_pad) {
+#pragma unroll
+            for (int kk = 8; kk < 16; ++kk) dim_step(kk);
+          }
+        } else {
+#pragma unroll(kUnrollKK)
+          for (int kk = 0; kk < BK; ++kk) dim_step(kk);
         }
         __syncwarp();  // every lane's reads of the stage are consumed
         if (lane == 0) {
@@ -405,15 +422,14 @@ cudaError_t launch_t(const CUtensorMap &map, int64_t tiles, int sms,
                      void *dist_out, int64_t ldd) {
   using C = typename Traits<DT>::C;
   using VT = typename VtOf<DT, VS>::T;
-  constexpr size_t sb = (size_t)stage_bytes<VT>();
+  constexpr size_t sb = (size_t)stage_bytes<VT, EG>();
   const size_t elem_bytes = (size_t)d_pad * EG * 8 * sizeof(C);
   // 8 KB stages: 5 / 6 / 8 per CTA at 4 / 3 / 2 CTAs per SM (about
   // 130-170 KB in flight per SM); deeper rings with fewer CTAs measured
-  // slower (13 stages at 2 CTAs: 0.150 vs 0.084 ms at k = 1).  The 4 KB
-  // stages of 2-byte V keep the same bytes in flight with twice the count.
+  // slower (13 stages at 2 CTAs: 0.150 vs 0.084 ms at k = 1).  4 KB stages
+  // (2-byte V, EG >= 4) keep the bytes in flight with twice the count.
   int nst = EG == 1 ? 5 : (EG == 2 ? 6 : 8);
-  if (sizeof(VT) == 2) nst *= 2;
-  if (nst > kMaxStages) nst = kMaxStages;
+  if (sb < (size_t)kStageBytes) nst = nst * 2 > kMaxStages ? kMaxStages : nst * 2;
   size_t smem = (size_t)nst * sb + elem_bytes;
   while (smem + 4096 > (size_t)kSmemPerSm && nst > 2) {
     --nst;
@@ -506,9 +522,11 @@ int set_min_tma(int dtype, const void *vt, int64_t ld, int64_t n, int d_pad,
   if (!set_min_tma_covers(dtype, d_pad, k, t_out != nullptr, vs)) return 1;
   const bool f64 = dtype == EXEM_F64;
   const int vb = f64 ? 8 : (vs ? 2 : 4);  // bytes per V value
-  const int bk = f64 ? bk_of<double>() : (vs ? bk_of<__half>() : bk_of<float>());
   int eg, et;
   choose(dtype, k, eg, et, vs);
+  const int bk = f64 ? bk_of<double, 1>()
+                     : (!vs ? bk_of<float, 1>()
+                            : (eg >= 4 ? bk_of<__half, 4>() : bk_of<__half, 1>()));
   CUtensorMap map;
   auto enc = tc::get_encode();
   if (!enc) return 1;

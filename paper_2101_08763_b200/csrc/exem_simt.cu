@@ -141,6 +141,72 @@ __global__ void __launch_bounds__(kRedThreads)
   if (threadIdx.x == 0) partials[blockIdx.x] = r;
 }
 
+// K1 for 2-byte storage written as 2-byte vt (EXEM_VT_STORAGE, even n):
+// 128 threads per 256 points, two adjacent points per thread, so every V
+// access is a 4-byte pair (a warp moves 128 contiguous bytes per dimension)
+// and the stored bits are copied untouched.  Per point the same sequential
+// fp64 norm / aux accumulation as ground_prepare_kernel, and the block
+// partial is block_sum<256>'s tree (pair_block_sum): bit-identical results.
+template <int DT>
+__global__ void __launch_bounds__(128)
+    ground_prepare_pair_kernel(const typename Traits<DT>::S *__restrict__ src,
+                               int64_t n, int d, int d_pad,
+                               const typename Traits<DT>::S *__restrict__ e0,
+                               typename Traits<DT>::S *__restrict__ vt,
+                               int64_t ld, double *__restrict__ norms,
+                               typename Traits<DT>::C *__restrict__ aux,
+                               double *__restrict__ partials, bool mark) {
+  using S = typename Traits<DT>::S;
+  using C = typename Traits<DT>::C;
+  __shared__ double sh[8];
+  const int64_t i = (int64_t)blockIdx.x * 256 + 2 * threadIdx.x;
+  const bool live = i < n;  // n even: both points of the pair or neither
+  double nrm[2] = {0.0, 0.0}, dst[2] = {0.0, 0.0};
+  auto accum = [&](uint32_t raw, int k) {
+    const S *h = reinterpret_cast<const S *>(&raw);
+    const double ek = (double)to_c(e0[k]);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const double xd = (double)to_c(h[q]);
+      nrm[q] += xd * xd;
+      const double df = xd - ek;
+      dst[q] += df * df;
+    }
+  };
+  constexpr int LA = 8;
+  int k = 0;
+  for (; k + LA <= d; k += LA) {
+    uint32_t xs[LA];
+#pragma unroll
+    for (int u = 0; u < LA; ++u)
+      xs[u] = live ? *reinterpret_cast<const uint32_t *>(src + (int64_t)(k + u) * n + i)
+                   : 0u;
+#pragma unroll
+    for (int u = 0; u < LA; ++u) {
+      *reinterpret_cast<uint32_t *>(vt + (int64_t)(k + u) * ld + i) = xs[u];
+      if (live) accum(xs[u], k + u);
+    }
+  }
+  for (; k < d_pad; ++k) {
+    uint32_t x = 0u;
+    if (k < d && live)
+      x = *reinterpret_cast<const uint32_t *>(src + (int64_t)k * n + i);
+    *reinterpret_cast<uint32_t *>(vt + (int64_t)k * ld + i) = x;
+    if (k < d && live) accum(x, k);
+  }
+  double part[2] = {0.0, 0.0};
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    C a = C(0);
+    if (live) a = (DT == EXEM_BF16) ? (C)dst[q] : to_c(from_d<S>(dst[q]));
+    norms[i + q] = live ? nrm[q] : 0.0;
+    aux[i + q] = a;
+    part[q] = live ? nonfinite_mark<DT>(mark, nrm[q], (double)a) : 0.0;
+  }
+  double r = pair_block_sum(part[0], part[1], sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = r;
+}
+
 // K1 for a row-major source (src[i][k], the C-order numpy matrix uploaded
 // as is): the block's 256 points are staged through shared memory 32
 // dimensions at a time (coalesced reads of the rows, conflict-free column
@@ -612,6 +678,114 @@ __global__ void __launch_bounds__(kRedThreads)
   }
   double r = block_sum<kRedThreads>(v, sh);
   if (threadIdx.x == 0) partials[blockIdx.x] = r;
+}
+
+// The m-update on 2-byte storage vt (EXEM_VT_STORAGE): two adjacent points
+// per thread (4-byte pair loads, 128 threads per 256 points), the same
+// per-point direct-form fma chain and xp refresh as greedy_update_kernel,
+// block partials by pair_block_sum (bit-identical).
+template <int DT>
+__global__ void __launch_bounds__(128)
+    greedy_update_pair_kernel(const typename Traits<DT>::S *__restrict__ vt,
+                              int64_t ld, int64_t n, int d,
+                              const double *__restrict__ norms,
+                              const typename Traits<DT>::S *__restrict__ cvt,
+                              int64_t ldc, const int64_t *__restrict__ sel_idx,
+                              int64_t step, float *__restrict__ m,
+                              typename Traits<DT>::S *__restrict__ xp,
+                              int64_t kp, double *__restrict__ partials) {
+  using S = typename Traits<DT>::S;
+  __shared__ double sh[8];
+  const int64_t c = sel_idx[step];
+  const int64_t i = (int64_t)blockIdx.x * 256 + 2 * threadIdx.x;
+  double v[2] = {0.0, 0.0};
+  if (i < n) {
+    const float2 m2 = *reinterpret_cast<const float2 *>(m + i);
+    float mi[2] = {m2.x, m2.y};
+    if (c >= 0) {  // c < 0: K5 found no valid candidate, S unchanged
+      float acc[2] = {0.f, 0.f};
+      auto step_k = [&](uint32_t raw, int k) {
+        const S *h = reinterpret_cast<const S *>(&raw);
+        const float y = to_c(cvt[(int64_t)k * ldc + c]);
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const float df = to_c(h[q]) - y;
+          acc[q] = fmaf(df, df, acc[q]);
+        }
+      };
+      constexpr int LA = 16;
+      int kk = 0;
+      for (; kk + LA <= d; kk += LA) {
+        uint32_t xs[LA];
+#pragma unroll
+        for (int u = 0; u < LA; ++u)
+          xs[u] = *reinterpret_cast<const uint32_t *>(vt + (int64_t)(kk + u) * ld + i);
+#pragma unroll
+        for (int u = 0; u < LA; ++u) step_k(xs[u], kk + u);
+      }
+      for (; kk < d; ++kk)
+        step_k(*reinterpret_cast<const uint32_t *>(vt + (int64_t)kk * ld + i), kk);
+#pragma unroll
+      for (int q = 0; q < 2; ++q) mi[q] = tmin(mi[q], acc[q]);
+      const bool two = i + 1 < n;
+      if (two) {
+        *reinterpret_cast<float2 *>(m + i) = make_float2(mi[0], mi[1]);
+      } else {
+        m[i] = mi[0];
+      }
+      if (xp != nullptr) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          if (q == 1 && !two) break;
+          double h[3];
+          fold_pieces<S>(0.5 * (norms[i + q] - (double)mi[q]), h);
+          S *row = xp + (i + q) * kp + d;
+          row[0] = from_d<S>(-h[0]);
+          row[1] = from_d<S>(-h[1]);
+          row[2] = from_d<S>(-h[2]);
+        }
+      }
+    }
+    v[0] = (double)mi[0];
+    v[1] = i + 1 < n ? (double)mi[1] : 0.0;
+  }
+  double r = pair_block_sum(v[0], v[1], sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = r;
+}
+
+// launchers of the pair kernels (half tags only; false for f32/f64)
+template <int DT>
+static bool launch_prepare_pair(int64_t blocks, cudaStream_t st,
+                                const void *src, int64_t n, int d, int d_pad,
+                                const void *e0, void *vt, int64_t ld,
+                                double *norms, void *aux, double *scratch,
+                                bool mark) {
+  if constexpr (DT == EXEM_F16 || DT == EXEM_BF16) {
+    using S = typename Traits<DT>::S;
+    using C = typename Traits<DT>::C;
+    ground_prepare_pair_kernel<DT><<<(unsigned)blocks, 128, 0, st>>>(
+        (const S *)src, n, d, d_pad, (const S *)e0, (S *)vt, ld, norms,
+        (C *)aux, scratch, mark);
+    return true;
+  }
+  return false;
+}
+
+template <int DT>
+static bool launch_update_pair(int64_t blocks, cudaStream_t st, const void *vt,
+                               int64_t ld, int64_t n, int d,
+                               const double *norms, const void *cvt,
+                               int64_t ldc, const int64_t *sel_idx,
+                               int64_t step, void *m, void *xp, int64_t kp,
+                               double *scratch) {
+  if constexpr (DT == EXEM_F16 || DT == EXEM_BF16) {
+    using S = typename Traits<DT>::S;
+    greedy_update_pair_kernel<DT><<<(unsigned)blocks, 128, 0, st>>>(
+        (const S *)vt, ld, n, d, norms, (const S *)cvt, ldc, sel_idx, step,
+        (float *)m, (S *)xp, kp, scratch);
+    return true;
+  }
+  return false;
 }
 
 // ============================================================ K3 / K4 SIMT
@@ -1295,6 +1469,13 @@ int exem_ground_prepare(int dtype, const void *src, int64_t n, int64_t d,
     using S = typename Traits<DT>::S;
     using C = typename Traits<DT>::C;
     using V = typename VtOf<DT, VS>::T;
+    // pair kernel for 2-byte vt: 4-byte aligned source rows need even n
+    if (VS && n % 2 == 0 &&
+        launch_prepare_pair<DT>(blocks, st, src, n, (int)d, d_pad, e0, vt, ld,
+                                norms, aux, scratch, check_finite != 0)) {
+      EXEM_LAUNCH_CHECK("ground_prepare_pair_kernel");
+      break;
+    }
     ground_prepare_kernel<DT, VS><<<(unsigned)blocks, kRedThreads, 0, st>>>(
         (const S *)src, n, (int)d, d_pad, (const S *)e0, (V *)vt, ld, norms,
         (C *)aux, scratch, check_finite != 0);
@@ -1424,6 +1605,12 @@ int exem_greedy_update(int dtype, const void *vt, int64_t ld, int64_t n,
     using S = typename Traits<DT>::S;
     using C = typename Traits<DT>::C;
     using V = typename VtOf<DT, VS>::T;
+    if (VS && launch_update_pair<DT>(blocks, st, vt, ld, n, (int)d, norms,
+                                     cvt, ldc, sel_idx, step, m, xp, kp,
+                                     scratch)) {
+      EXEM_LAUNCH_CHECK("greedy_update_pair_kernel");
+      break;
+    }
     greedy_update_kernel<DT, VS><<<(unsigned)blocks, kRedThreads, 0, st>>>(
         (const V *)vt, ld, n, (int)d, norms, (const V *)cvt, ldc, cnorms,
         sel_idx, step, (C *)m, (S *)xp, kp, scratch);

@@ -48,6 +48,42 @@ def test_vt_is_two_byte_and_widening_exact(prec):
 
 
 @pytest.mark.parametrize("prec", HALVES, ids=lambda p: p.value)
+@pytest.mark.parametrize("n", [3000, 3001, 256, 1])
+@pytest.mark.parametrize("rows", [False, True], ids=["colmajor", "rowmajor"])
+def test_k1_storage_bit_equal(prec, n, rows):
+    """K1 writing 2-byte vt (the pair kernel for even n, the one-point
+    kernel for odd n; the row-major transpose) equals K1 writing the
+    binary32 widening: norms, aux, the fixed-order aux sum, and vt."""
+    import torch
+
+    from paper_2101_08763_b200.device import to_device_bytes
+
+    d = 37
+    g, _ = _ground(prec, n, d, seed=n)
+    dg = g.on_device()
+    lib = N.lib()
+    st = dg.stream
+    host = np.ascontiguousarray(g.matrix) if rows else \
+        np.asfortranarray(g.matrix)
+    src = to_device_bytes(host.ravel(order="C" if rows else "F"), dg.dev)
+    e0 = to_device_bytes(g.aux, dg.dev)
+    prep = lib.ground_prepare_rows if rows else lib.ground_prepare
+    out = []
+    for tag, vdt in ((dg.vt_tag, dg.vt.dtype), (prec.tag, torch.float32)):
+        vt = torch.full((dg.d_pad, dg.ld), 7, dtype=vdt, device=dg.dev)
+        norms = torch.empty(dg.ld, dtype=torch.float64, device=dg.dev)
+        aux = torch.empty(dg.ld, dtype=torch.float32, device=dg.dev)
+        s = torch.empty(1, dtype=torch.float64, device=dg.dev)
+        prep(tag, N.ptr(src), n, d, N.ptr(e0), N.ptr(vt), dg.ld, N.ptr(norms),
+             N.ptr(aux), N.ptr(s), N.ptr(dg.scratch), 1, st)
+        out.append((vt.float().cpu(), norms.cpu(), aux.cpu(), s.item()))
+    (v0, n0, a0, s0), (v1, n1, a1, s1) = out
+    assert torch.equal(v0, v1)
+    assert torch.equal(n0, n1) and torch.equal(a0, a1)
+    assert s0 == s1
+
+
+@pytest.mark.parametrize("prec", HALVES, ids=lambda p: p.value)
 @pytest.mark.parametrize("n,d,k", [(5000, 100, 1), (5000, 100, 10),
                                    (4099, 37, 50), (4099, 100, 64),
                                    (3000, 16, 100), (2000, 300, 20)])

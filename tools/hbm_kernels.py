@@ -147,18 +147,21 @@ def main():
         m.copy_(dg.aux)
         sel = torch.zeros(1, dtype=torch.int64, device=dg.dev)
         msum = torch.empty(1, dtype=torch.float64, device=dg.dev)
-        xp = None
+        variants = [(None, "m only")]
         if half:  # the Greedy's TC point operand (its h columns refreshed)
-            xp = torch.zeros((int(lib.tc_rows(n)), dg.kp), dtype=dg.vt.dtype,
-                             device=dg.dev)
-        t = timed(lambda: lib.greedy_update(
-            tag, N.ptr(dg.vt), dg.ld, n, d, N.ptr(dg.norms),
-            N.ptr(dg.vt), dg.ld, N.ptr(dg.norms), N.ptr(sel), 0, N.ptr(m),
-            N.ptr(xp), dg.kp if half else 0, N.ptr(msum), N.ptr(dg.scratch),
-            st))
-        rec(f"K2 greedy_update (m-update, {prec.value}, vt {vb}-byte)",
-            n * d * vb + 20 * n + (6 * n if half else 0), t, 2.0 * n * d,
-            instr)
+            variants.append((torch.zeros((int(lib.tc_rows(n)), dg.kp),
+                                         dtype=dg.vt.dtype, device=dg.dev),
+                             "with the TC h refresh"))
+        for xp, what in variants:
+            t = timed(lambda: lib.greedy_update(
+                tag, N.ptr(dg.vt), dg.ld, n, d, N.ptr(dg.norms),
+                N.ptr(dg.vt), dg.ld, N.ptr(dg.norms), N.ptr(sel), 0, N.ptr(m),
+                N.ptr(xp), dg.kp if xp is not None else 0, N.ptr(msum),
+                N.ptr(dg.scratch), st))
+            rec(f"K2 greedy_update (m-update, {prec.value}, vt {vb}-byte, "
+                f"{what})",
+                n * d * vb + 20 * n + (6 * n if xp is not None else 0), t,
+                2.0 * n * d, instr)
     # .exem loader straight to the device (io.py: mapped payload -> one DMA
     # -> K1), wall clock of the public load_ground_set, file bytes / time
     import tempfile
