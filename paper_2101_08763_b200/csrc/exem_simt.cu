@@ -17,6 +17,8 @@
 
 #include <cstring>
 
+#include <cstdlib>
+
 #include "exem_common.cuh"
 
 namespace exem {
@@ -678,6 +680,133 @@ __global__ void __launch_bounds__(kRedThreads)
   }
   double r = block_sum<kRedThreads>(v, sh);
   if (threadIdx.x == 0) partials[blockIdx.x] = r;
+}
+
+// K1 for a row-major source whose 256-row slab fits in shared memory
+// (2- and 4-byte storage): the block's rows are one contiguous run of
+// 256*d values, copied with 16-byte loads (full 128-byte lines, every byte
+// read once) into rows of odd word pitch (conflict-free column reads), then
+// the per-point arithmetic and block partials of ground_prepare_kernel --
+// bit-identical.  (The 32-dimension tiles of ground_prepare_rows_kernel read
+// each row in 64/128-byte pieces that straddle sectors: 0.21-0.48 of HBM.)
+constexpr int kSlabMaxBytes = 112 * 1024;  // two CTAs per SM
+template <typename S> __host__ __device__ constexpr int slab_pitch(int d) {
+  // elements per smem row: an odd number of 4-byte words
+  return sizeof(S) == 4 ? (d | 1) : ((((d + 1) / 2) | 1) * 2);
+}
+
+template <int DT, bool VS>
+__global__ void __launch_bounds__(kRedThreads)
+    ground_prepare_slab_kernel(const typename Traits<DT>::S *__restrict__ src,
+                               int64_t n, int d, int d_pad,
+                               const typename Traits<DT>::S *__restrict__ e0,
+                               typename VtOf<DT, VS>::T *__restrict__ vt,
+                               int64_t ld, double *__restrict__ norms,
+                               typename Traits<DT>::C *__restrict__ aux,
+                               double *__restrict__ partials, bool mark) {
+  using S = typename Traits<DT>::S;
+  using C = typename Traits<DT>::C;
+  using V = typename VtOf<DT, VS>::T;
+  constexpr int per = 16 / (int)sizeof(S);  // values per 16-byte load
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  S *slab = reinterpret_cast<S *>(smem_raw);  // [256][P]
+  __shared__ double sh[32];
+  const int P = slab_pitch<S>(d);
+  const int64_t i0 = (int64_t)blockIdx.x * kRedThreads;
+  const int rows = (int)min((int64_t)kRedThreads, n - i0);  // >= 1 (ld < n + 256)
+  const int64_t total = (int64_t)rows * d;  // values of the slab
+  const S *g = src + i0 * d;                // 16-byte aligned (256*d*sizeof(S))
+  const int64_t nv = total / per;
+  // running (row, col) of value idx*per, advanced by 256*per per iteration
+  const int step = kRedThreads * per;
+  int r = (int)(((int64_t)threadIdx.x * per) / d);
+  int c = (int)(((int64_t)threadIdx.x * per) - (int64_t)r * d);
+  const int dq = step / d, dr = step - dq * d;
+  // kU independent 16-byte loads in flight per thread, then their scatter
+  constexpr int kU = 8;
+  auto scatter = [&](const uint4 &q) {
+    const S *qs = reinterpret_cast<const S *>(&q);
+    int rr = r, cc = c;
+#pragma unroll
+    for (int j = 0; j < per; ++j) {
+      slab[rr * P + cc] = qs[j];
+      if (++cc == d) {
+        cc = 0;
+        ++rr;
+      }
+    }
+    r += dq;
+    c += dr;
+    if (c >= d) {
+      c -= d;
+      ++r;
+    }
+  };
+  int64_t idx = threadIdx.x;
+  for (; idx + (kU - 1) * kRedThreads < nv; idx += kU * kRedThreads) {
+    uint4 q[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      q[u] = __ldg(reinterpret_cast<const uint4 *>(g) + idx + u * kRedThreads);
+#pragma unroll
+    for (int u = 0; u < kU; ++u) scatter(q[u]);
+  }
+  for (; idx < nv; idx += kRedThreads)
+    scatter(__ldg(reinterpret_cast<const uint4 *>(g) + idx));
+  for (int64_t e = nv * per + threadIdx.x; e < total; e += kRedThreads) {
+    const int rr = (int)(e / d);
+    slab[rr * P + (int)(e - (int64_t)rr * d)] = g[e];
+  }
+  __syncthreads();
+  const int64_t i = i0 + threadIdx.x;
+  const bool live = threadIdx.x < rows;
+  double nrm = 0.0, dst = 0.0;
+  const S *row = slab + threadIdx.x * P;
+  for (int k = 0; k < d_pad; ++k) {
+    C x = C(0);
+    if (k < d && live) x = to_c(row[k]);
+    vt[(int64_t)k * ld + i] = to_vt<V>(x);
+    if (k < d && live) {
+      const double xd = (double)x;
+      nrm += xd * xd;
+      const double df = xd - (double)to_c(e0[k]);
+      dst += df * df;
+    }
+  }
+  C a = C(0);
+  if (live) a = (DT == EXEM_BF16) ? (C)dst : to_c(from_d<S>(dst));
+  norms[i] = live ? nrm : 0.0;
+  aux[i] = a;
+  dst = live ? nonfinite_mark<DT>(mark, nrm, (double)a) : 0.0;
+  double rs = block_sum<kRedThreads>(dst, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = rs;
+}
+
+// 0 launched, 1 not applicable (8-byte values, or the slab does not fit),
+// < 0 a CUDA error
+template <int DT, bool VS>
+static int launch_prepare_slab(int64_t blocks, cudaStream_t st,
+                               const void *src, int64_t n, int d, int d_pad,
+                               const void *e0, void *vt, int64_t ld,
+                               double *norms, void *aux, double *scratch,
+                               bool mark) {
+  using S = typename Traits<DT>::S;
+  if constexpr (sizeof(S) <= 4) {
+    using C = typename Traits<DT>::C;
+    using V = typename VtOf<DT, VS>::T;
+    const size_t slab = (size_t)kRedThreads * slab_pitch<S>(d) * sizeof(S);
+    if (slab > (size_t)kSlabMaxBytes || getenv("EXEM_K1_TILES")) return 1;
+    cudaError_t e = cudaFuncSetAttribute(
+        ground_prepare_slab_kernel<DT, VS>,
+        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)slab);
+    if (e != cudaSuccess) return -(int)e;
+    ground_prepare_slab_kernel<DT, VS><<<(unsigned)blocks, kRedThreads, slab,
+                                         st>>>(
+        (const S *)src, n, d, d_pad, (const S *)e0, (V *)vt, ld, norms,
+        (C *)aux, scratch, mark);
+    return 0;
+  }
+  return 1;
 }
 
 // The m-update on 2-byte storage vt (EXEM_VT_STORAGE): two adjacent points
@@ -2030,6 +2159,19 @@ int exem_ground_prepare_rows(int dtype, const void *src, int64_t n, int64_t d,
     using S = typename Traits<DT>::S;
     using C = typename Traits<DT>::C;
     using V = typename VtOf<DT, VS>::T;
+    {
+      const int rc = launch_prepare_slab<DT, VS>(blocks, st, src, n, (int)d,
+                                                 d_pad, e0, vt, ld, norms,
+                                                 aux, scratch,
+                                                 check_finite != 0);
+      if (rc < 0)
+        return fail(EXEM_ERR_CUDA, "prepare_rows smem: %s",
+                    cudaGetErrorString((cudaError_t)(-rc)));
+      if (rc == 0) {
+        EXEM_LAUNCH_CHECK("ground_prepare_slab_kernel");
+        break;
+      }
+    }
     const size_t smem = (size_t)kRedThreads * 33 * sizeof(C);
     if (smem > 48 * 1024) {
       cudaError_t e = cudaFuncSetAttribute(

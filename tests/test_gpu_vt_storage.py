@@ -47,40 +47,48 @@ def test_vt_is_two_byte_and_widening_exact(prec):
     assert np.array_equal(dg.column_major_storage(), g.matrix)
 
 
-@pytest.mark.parametrize("prec", HALVES, ids=lambda p: p.value)
-@pytest.mark.parametrize("n", [3000, 3001, 256, 1])
-@pytest.mark.parametrize("rows", [False, True], ids=["colmajor", "rowmajor"])
-def test_k1_storage_bit_equal(prec, n, rows):
-    """K1 writing 2-byte vt (the pair kernel for even n, the one-point
-    kernel for odd n; the row-major transpose) equals K1 writing the
-    binary32 widening: norms, aux, the fixed-order aux sum, and vt."""
+@pytest.mark.parametrize("prec", HALVES + [pb.Precision.binary32],
+                         ids=lambda p: p.value)
+@pytest.mark.parametrize("n,d", [(3000, 37), (3001, 37), (256, 100), (1, 5),
+                                 (2999, 100), (1000, 220), (700, 400)])
+def test_k1_layouts_bit_equal(prec, n, d):
+    """K1 over every source layout and vt element type gives the same
+    norms, aux, fixed-order aux sum and vt: column-major source (the pair
+    kernel for even n with 2-byte vt, the one-point kernel otherwise) and
+    row-major source (the shared-memory slab kernel, or the 32-dimension
+    tile kernel when the slab does not fit), each writing 2-byte or
+    binary32 vt."""
     import torch
 
     from paper_2101_08763_b200.device import to_device_bytes
 
-    d = 37
-    g, _ = _ground(prec, n, d, seed=n)
+    g, _ = _ground(prec, n, d, seed=n + d)
     dg = g.on_device()
     lib = N.lib()
     st = dg.stream
-    host = np.ascontiguousarray(g.matrix) if rows else \
-        np.asfortranarray(g.matrix)
-    src = to_device_bytes(host.ravel(order="C" if rows else "F"), dg.dev)
     e0 = to_device_bytes(g.aux, dg.dev)
-    prep = lib.ground_prepare_rows if rows else lib.ground_prepare
+    tags = [(prec.tag, torch.float32)]
+    if dg.vt_flag:
+        tags.append((dg.vt_tag, dg.vt.dtype))
     out = []
-    for tag, vdt in ((dg.vt_tag, dg.vt.dtype), (prec.tag, torch.float32)):
-        vt = torch.full((dg.d_pad, dg.ld), 7, dtype=vdt, device=dg.dev)
-        norms = torch.empty(dg.ld, dtype=torch.float64, device=dg.dev)
-        aux = torch.empty(dg.ld, dtype=torch.float32, device=dg.dev)
-        s = torch.empty(1, dtype=torch.float64, device=dg.dev)
-        prep(tag, N.ptr(src), n, d, N.ptr(e0), N.ptr(vt), dg.ld, N.ptr(norms),
-             N.ptr(aux), N.ptr(s), N.ptr(dg.scratch), 1, st)
-        out.append((vt.float().cpu(), norms.cpu(), aux.cpu(), s.item()))
-    (v0, n0, a0, s0), (v1, n1, a1, s1) = out
-    assert torch.equal(v0, v1)
-    assert torch.equal(n0, n1) and torch.equal(a0, a1)
-    assert s0 == s1
+    for rows in (False, True):
+        host = np.ascontiguousarray(g.matrix) if rows else \
+            np.asfortranarray(g.matrix)
+        src = to_device_bytes(host.ravel(order="C" if rows else "F"), dg.dev)
+        prep = lib.ground_prepare_rows if rows else lib.ground_prepare
+        for tag, vdt in tags:
+            vt = torch.full((dg.d_pad, dg.ld), 7, dtype=vdt, device=dg.dev)
+            norms = torch.empty(dg.ld, dtype=torch.float64, device=dg.dev)
+            aux = torch.empty(dg.ld, dtype=torch.float32, device=dg.dev)
+            s = torch.empty(1, dtype=torch.float64, device=dg.dev)
+            prep(tag, N.ptr(src), n, d, N.ptr(e0), N.ptr(vt), dg.ld,
+                 N.ptr(norms), N.ptr(aux), N.ptr(s), N.ptr(dg.scratch), 1, st)
+            out.append((vt.float().cpu(), norms.cpu(), aux.cpu(), s.item()))
+    v0, n0, a0, s0 = out[0]
+    for v1, n1, a1, s1 in out[1:]:
+        assert torch.equal(v0, v1)
+        assert torch.equal(n0, n1) and torch.equal(a0, a1)
+        assert s0 == s1
 
 
 @pytest.mark.parametrize("prec", HALVES, ids=lambda p: p.value)
