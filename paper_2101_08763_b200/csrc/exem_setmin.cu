@@ -288,9 +288,33 @@ __global__ void __launch_bounds__(kThreads, min_ctas<EG>())
             for (int w = 0; w < per; ++w) ev[u + w] = qc[w];
           }
 #pragma unroll
-          for (int p = 0; p < PT; ++p)
+          for (int p = 0; p < PT; ++p) {
+#ifndef EXEM_K2_NO_FFMA2
+            // binary32 compute: element pairs through FFMA2 (/ FADD2) with
+            // the point as the broadcast operand -- per lane the same IEEE
+            // fma / sub as the scalar form (bit-identical), half the issues
+            constexpr int JP = sizeof(C) == 4 ? (ET & ~1) : 0;
+            if constexpr (JP > 0) {
+              const float2 pp = make_float2(pv[p], pv[p]);
 #pragma unroll
-            for (int j = 0; j < ET; ++j) {
+              for (int j = 0; j < JP; j += 2) {
+                float2 t = make_float2(acc[p][j], acc[p][j + 1]);
+                if constexpr (Traits<DT>::kDirect) {
+                  const float2 df =
+                      __fadd2_rn(pp, make_float2(-ev[j], -ev[j + 1]));
+                  t = __ffma2_rn(df, df, t);
+                } else {
+                  t = __ffma2_rn(pp, make_float2(ev[j], ev[j + 1]), t);
+                }
+                acc[p][j] = t.x;
+                acc[p][j + 1] = t.y;
+              }
+            }
+#else
+            constexpr int JP = 0;
+#endif
+#pragma unroll
+            for (int j = JP; j < ET; ++j) {
               if constexpr (Traits<DT>::kDirect) {
                 const C df = pv[p] - ev[j];
                 acc[p][j] = fma(df, df, acc[p][j]);
@@ -298,6 +322,7 @@ __global__ void __launch_bounds__(kThreads, min_ctas<EG>())
                 acc[p][j] = fma(pv[p], ev[j], acc[p][j]);
               }
             }
+          }
         };
         if constexpr (BK == 16) {  // 2-byte V: 8 dims, then 8 more unless tail
 #pragma unroll

@@ -959,6 +959,31 @@ __device__ __forceinline__ void mma_chunk(const SimtSmem<T, BK> &sm, int buf,
       b[r] = sm.b[buf][kk][tx * 4 + r];
       b[4 + r] = sm.b[buf][kk][64 + tx * 4 + r];
     }
+#ifndef EXEM_SIMT_NO_FFMA2
+    // binary32: paired FFMA2 (/ FADD2) with a[r] as the broadcast operand --
+    // per lane the same IEEE fma (sub) as the scalar loop, so results are
+    // bit-identical, at half the issue slots (C2 39.5 -> 35.7 ms per step,
+    // profiles/r02_ffma2_ab.log)
+    if constexpr (sizeof(T) == 4) {
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const float2 ar = make_float2(a[r], a[r]);
+#pragma unroll
+        for (int c = 0; c < 8; c += 2) {
+          float2 t = make_float2(acc[r][c], acc[r][c + 1]);
+          if constexpr (kDirect) {
+            const float2 df = __fadd2_rn(ar, make_float2(-b[c], -b[c + 1]));
+            t = __ffma2_rn(df, df, t);
+          } else {
+            t = __ffma2_rn(ar, make_float2(b[c], b[c + 1]), t);
+          }
+          acc[r][c] = t.x;
+          acc[r][c + 1] = t.y;
+        }
+      }
+      continue;
+    }
+#endif
 #pragma unroll
     for (int r = 0; r < 8; ++r)
 #pragma unroll
