@@ -1,3 +1,9 @@
+"""Same-box A/B of the paired FFMA2 outer product (K3-SIMT binary32, C2 /
+C3 fp32 shapes): the shipped library vs an experiment build without it.
+
+    tools/build_ab.sh nof2="-DEXEM_SIMT_NO_FFMA2 -DEXEM_K2_NO_FFMA2"
+    python tools/ffma2_ab.py        # on the GPU box (gpurun)
+"""
 import json, os, subprocess, sys
 from pathlib import Path
 ROOT = Path("/root/repo")
