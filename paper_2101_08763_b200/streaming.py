@@ -41,15 +41,19 @@ def _csize(precision) -> int:
 
 
 def layout_bytes(rows: int, d: int, precision, with_src: bool = False,
-                 tc_operands: int = 1) -> int:
+                 tc_operands: int = 1, vt_storage: bool = False) -> int:
     """Device bytes of the layouts of ``rows`` points:
     SIMT vt + norms + aux, plus ``tc_operands`` half operands for the
-    half precisions, plus the raw upload buffer when ``with_src``."""
+    half precisions, plus the raw upload buffer when ``with_src``.
+    ``vt_storage``: vt at the 2-byte storage type of a half ground set (the
+    resident layout, EXEM_VT_STORAGE); streamed slots keep it widened."""
     lib = N.lib()
     ld = int(lib.pad_points(rows))
     d_pad = int(lib.pad_dims(d))
     cs = _csize(precision)
-    b = d_pad * ld * cs + ld * 8 + ld * cs
+    vs = precision.bytes_per_value if (vt_storage and precision.is_half) \
+        else cs
+    b = d_pad * ld * vs + ld * 8 + ld * cs
     if precision.is_half:
         kp = max(int(lib.tc_kp(d)), int(lib.tc_batch_kp(d)))
         b += tc_operands * int(lib.tc_rows(rows)) * kp * 2
@@ -61,7 +65,7 @@ def layout_bytes(rows: int, d: int, precision, with_src: bool = False,
 def resident_bytes(n: int, d: int, precision) -> int:
     """Bytes of a fully resident ground set (incl. the reduction scratch)."""
     lib = N.lib()
-    return (layout_bytes(n, d, precision, tc_operands=2) +
+    return (layout_bytes(n, d, precision, tc_operands=2, vt_storage=True) +
             int(lib.reduce_scratch(int(lib.pad_points(n)))) * 8)
 
 
