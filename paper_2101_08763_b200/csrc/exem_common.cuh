@@ -38,6 +38,9 @@ constexpr int kTcConst = 6;     // folded constant columns in the TC operands
 constexpr int kTcKChunk = 64;   // bf16/f16 elements per 128-byte swizzle row
 
 inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+inline bool aligned(const void *p, uintptr_t a) {
+  return ((uintptr_t)p & (a - 1)) == 0;
+}
 inline int64_t ceil_div(int64_t x, int64_t m) { return (x + m - 1) / m; }
 
 // ---------------------------------------------------------------- types

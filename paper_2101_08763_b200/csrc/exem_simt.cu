@@ -795,7 +795,9 @@ static int launch_prepare_slab(int64_t blocks, cudaStream_t st,
     using C = typename Traits<DT>::C;
     using V = typename VtOf<DT, VS>::T;
     const size_t slab = (size_t)kRedThreads * slab_pitch<S>(d) * sizeof(S);
-    if (slab > (size_t)kSlabMaxBytes || getenv("EXEM_K1_TILES")) return 1;
+    if (slab > (size_t)kSlabMaxBytes || !aligned(src, 16) ||
+        getenv("EXEM_K1_TILES"))
+      return 1;
     cudaError_t e = cudaFuncSetAttribute(
         ground_prepare_slab_kernel<DT, VS>,
         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)slab);
@@ -964,7 +966,11 @@ __device__ __forceinline__ void mma_chunk(const SimtSmem<T, BK> &sm, int buf,
     // per lane the same IEEE fma (sub) as the scalar loop, so results are
     // bit-identical, at half the issue slots (C2 39.5 -> 35.7 ms per step,
     // profiles/r02_ffma2_ab.log)
-    if constexpr (sizeof(T) == 4) {
+    constexpr bool kPaired = sizeof(T) == 4;
+#else
+    constexpr bool kPaired = false;
+#endif
+    if constexpr (kPaired) {
 #pragma unroll
       for (int r = 0; r < 8; ++r) {
         const float2 ar = make_float2(a[r], a[r]);
@@ -981,20 +987,19 @@ __device__ __forceinline__ void mma_chunk(const SimtSmem<T, BK> &sm, int buf,
           acc[r][c + 1] = t.y;
         }
       }
-      continue;
-    }
-#endif
+    } else {
 #pragma unroll
-    for (int r = 0; r < 8; ++r)
+      for (int r = 0; r < 8; ++r)
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        if (kDirect) {
-          const T df = a[r] - b[c];
-          acc[r][c] = fma(df, df, acc[r][c]);
-        } else {
-          acc[r][c] = fma(a[r], b[c], acc[r][c]);
+        for (int c = 0; c < 8; ++c) {
+          if (kDirect) {
+            const T df = a[r] - b[c];
+            acc[r][c] = fma(df, df, acc[r][c]);
+          } else {
+            acc[r][c] = fma(a[r], b[c], acc[r][c]);
+          }
         }
-      }
+    }
   }
 }
 
@@ -1624,7 +1629,8 @@ int exem_ground_prepare(int dtype, const void *src, int64_t n, int64_t d,
     using C = typename Traits<DT>::C;
     using V = typename VtOf<DT, VS>::T;
     // pair kernel for 2-byte vt: 4-byte aligned source rows need even n
-    if (VS && n % 2 == 0 &&
+    // (and 4-byte aligned buffers)
+    if (VS && n % 2 == 0 && aligned(src, 4) && aligned(vt, 4) &&
         launch_prepare_pair<DT>(blocks, st, src, n, (int)d, d_pad, e0, vt, ld,
                                 norms, aux, scratch, check_finite != 0)) {
       EXEM_LAUNCH_CHECK("ground_prepare_pair_kernel");
@@ -1759,7 +1765,8 @@ int exem_greedy_update(int dtype, const void *vt, int64_t ld, int64_t n,
     using S = typename Traits<DT>::S;
     using C = typename Traits<DT>::C;
     using V = typename VtOf<DT, VS>::T;
-    if (VS && launch_update_pair<DT>(blocks, st, vt, ld, n, (int)d, norms,
+    if (VS && aligned(vt, 4) && aligned(cvt, 2) && aligned(m, 8) &&
+        launch_update_pair<DT>(blocks, st, vt, ld, n, (int)d, norms,
                                      cvt, ldc, sel_idx, step, m, xp, kp,
                                      scratch)) {
       EXEM_LAUNCH_CHECK("greedy_update_pair_kernel");

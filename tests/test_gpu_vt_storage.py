@@ -51,13 +51,15 @@ def test_vt_is_two_byte_and_widening_exact(prec):
                          ids=lambda p: p.value)
 @pytest.mark.parametrize("n,d", [(3000, 37), (3001, 37), (256, 100), (1, 5),
                                  (2999, 100), (1000, 220), (700, 400)])
-def test_k1_layouts_bit_equal(prec, n, d):
+@pytest.mark.parametrize("misalign", [False, True], ids=["aligned", "offset"])
+def test_k1_layouts_bit_equal(prec, n, d, misalign):
     """K1 over every source layout and vt element type gives the same
     norms, aux, fixed-order aux sum and vt: column-major source (the pair
     kernel for even n with 2-byte vt, the one-point kernel otherwise) and
     row-major source (the shared-memory slab kernel, or the 32-dimension
     tile kernel when the slab does not fit), each writing 2-byte or
-    binary32 vt."""
+    binary32 vt.  ``offset``: the source starts one value past a 16-byte
+    boundary (the pair / slab kernels step aside for the scalar ones)."""
     import torch
 
     from paper_2101_08763_b200.device import to_device_bytes
@@ -74,14 +76,18 @@ def test_k1_layouts_bit_equal(prec, n, d):
     for rows in (False, True):
         host = np.ascontiguousarray(g.matrix) if rows else \
             np.asfortranarray(g.matrix)
-        src = to_device_bytes(host.ravel(order="C" if rows else "F"), dg.dev)
+        raw = to_device_bytes(host.ravel(order="C" if rows else "F"), dg.dev)
+        off = prec.bytes_per_value if misalign else 0
+        buf = torch.zeros(raw.numel() + 16, dtype=torch.uint8, device=dg.dev)
+        buf[off:off + raw.numel()].copy_(raw)
+        src = N.c_void_p(buf.data_ptr() + off)
         prep = lib.ground_prepare_rows if rows else lib.ground_prepare
         for tag, vdt in tags:
             vt = torch.full((dg.d_pad, dg.ld), 7, dtype=vdt, device=dg.dev)
             norms = torch.empty(dg.ld, dtype=torch.float64, device=dg.dev)
             aux = torch.empty(dg.ld, dtype=torch.float32, device=dg.dev)
             s = torch.empty(1, dtype=torch.float64, device=dg.dev)
-            prep(tag, N.ptr(src), n, d, N.ptr(e0), N.ptr(vt), dg.ld,
+            prep(tag, src, n, d, N.ptr(e0), N.ptr(vt), dg.ld,
                  N.ptr(norms), N.ptr(aux), N.ptr(s), N.ptr(dg.scratch), 1, st)
             out.append((vt.float().cpu(), norms.cpu(), aux.cpu(), s.item()))
     v0, n0, a0, s0 = out[0]
