@@ -1139,7 +1139,7 @@ struct BatchSmem {
   T px[kBN];   // point aux distances of the tile
 };
 
-template <int DT>
+template <int DT, bool kTail = false>
 __global__ void __launch_bounds__(kThreads, (DT == EXEM_F64 ? 1 : 2))
     batch_eval_kernel(const typename Traits<DT>::C *__restrict__ vt,
                       int64_t ld, int64_t n, int d_pad, int d,
@@ -1194,8 +1194,10 @@ __global__ void __launch_bounds__(kThreads, (DT == EXEM_F64 ? 1 : 2))
 #pragma unroll
         for (int c = 0; c < 8; ++c) acc[r][c] = T(0);
       // element e of sets j0..j0+127 at dim k: packed[k*ldp + e*l_pad + j]
-      simt_mainloop<T, kDirect>(sm.mm, packed + (int64_t)e * l_pad, ldp, j0,
-                                vt, ld, p0, d_pad, d, tx, ty, acc);
+      simt_mainloop<T, kDirect, kBK, kTail>(sm.mm,
+                                            packed + (int64_t)e * l_pad, ldp,
+                                            j0, vt, ld, p0, d_pad, d, tx, ty,
+                                            acc);
 #pragma unroll
       for (int r = 0; r < 8; ++r) {
         const int jr = tile_off(ty, r);
@@ -1918,15 +1920,25 @@ int exem_batch_eval(int dtype, const void *vt, int64_t ld, int64_t n,
   EXEM_DISPATCH(dtype, DT, {
     using C = typename Traits<DT>::C;
     size_t smem = sizeof(BatchSmem<C>);
+    // partial last chunk (d % 8 != 0): the instantiation that skips its
+    // zero padding dimensions (exact zeros; see simt_mainloop)
+    const bool tail = d % kBK != 0;
     cudaError_t e = cudaFuncSetAttribute(
-        batch_eval_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-        (int)smem);
+        tail ? (const void *)batch_eval_kernel<DT, true>
+             : (const void *)batch_eval_kernel<DT, false>,
+        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess)
       return fail(EXEM_ERR_CUDA, "batch_eval smem: %s", cudaGetErrorString(e));
-    batch_eval_kernel<DT><<<grid, kThreads, smem, st>>>(
-        (const C *)vt, ld, n, d_pad, (int)d, norms, (const C *)aux,
-        (const C *)packed,
-        pnorms, card, l, l_pad, (int)k_max, split_pts, partial);
+    if (tail)
+      batch_eval_kernel<DT, true><<<grid, kThreads, smem, st>>>(
+          (const C *)vt, ld, n, d_pad, (int)d, norms, (const C *)aux,
+          (const C *)packed, pnorms, card, l, l_pad, (int)k_max, split_pts,
+          partial);
+    else
+      batch_eval_kernel<DT, false><<<grid, kThreads, smem, st>>>(
+          (const C *)vt, ld, n, d_pad, (int)d, norms, (const C *)aux,
+          (const C *)packed, pnorms, card, l, l_pad, (int)k_max, split_pts,
+          partial);
     EXEM_LAUNCH_CHECK("batch_eval_kernel");
   });
   return EXEM_OK;
