@@ -309,6 +309,26 @@ def test_stream_plan_is_split_aligned(native_lib):
         assert not S.fits_resident(n, d, prec, S.resident_bytes(n, d, prec) - 1)
 
 
+def test_resident_bytes_count_two_byte_vt(native_lib):
+    """Resident half ground sets keep vt at the 2-byte storage type
+    (EXEM_VT_STORAGE); streamed slots keep the binary32 widening."""
+    from paper_2101_08763_b200 import streaming as S
+
+    P = pb.Precision
+    n, d = 1_000_000, 100
+    ld = int(native_lib.pad_points(n))
+    d_pad = int(native_lib.pad_dims(d))
+    for prec in (P.bfloat16, P.binary16):
+        wide = S.layout_bytes(n, d, prec)
+        narrow = S.layout_bytes(n, d, prec, vt_storage=True)
+        assert wide - narrow == d_pad * ld * 2
+    for prec in (P.binary32, P.binary64):  # no storage flag for wide types
+        assert S.layout_bytes(n, d, prec) == \
+            S.layout_bytes(n, d, prec, vt_storage=True)
+    # C4 bf16: vt 208 MB + two half operands + norms/aux + scratch < 1 GB
+    assert S.resident_bytes(n, d, P.bfloat16) < 1.0e9
+
+
 def test_tc_set_geometry(native_lib):
     """K4-TC set tiles: w = k_max slots per set (column-interleaved), as many
     sets as fit 256 TMEM columns (<= 16; <= 32 in the small-set kernel,
