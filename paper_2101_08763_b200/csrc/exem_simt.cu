@@ -1845,12 +1845,15 @@ int exem_greedy_gains_simt(int dtype, const void *cvt, int64_t ldc,
   }
   dim3 grid((unsigned)ceil_div(l, kBM), (unsigned)splits);
   // fp64: k-chunks of 16 (half the ring barriers per DFMA) when d_pad allows
-  // it without extra padding -- d = 512 / 1024: 436 -> 413 / 866 -> 822 ms;
-  // fp32 measured slower that way (0.75 -> 0.73 of FFMA), kept at 8.
+  // it without extra padding -- d = 512 / 1024: 436 -> 413 / 866 -> 822 ms.
+  // fp32 with the paired FFMA2 loop: 16 from d_pad = 128 up (d = 512 / 1024:
+  // 169.5 -> 167.2 / 337.5 -> 333.1 ms); small d keeps 8 (d = 16: 6.82 vs
+  // 6.93 ms) (profiles/r02_simt_bk.log).
   // EXEM_SIMT_BK = 8 | 16 overrides (timing experiments).
   static const int bk_env = getenv("EXEM_SIMT_BK") ? atoi(getenv("EXEM_SIMT_BK")) : 0;
   const bool bk16 = d_pad % 16 == 0 &&
-                    (bk_env == 16 || (bk_env == 0 && dtype == EXEM_F64));
+                    (bk_env == 16 ||
+                     (bk_env == 0 && (dtype == EXEM_F64 || d_pad >= 128)));
   if (dtype == EXEM_F32 && bk16) {
     size_t smem = sizeof(SimtSmem<float, 16>);
     cudaError_t e = cudaFuncSetAttribute(
